@@ -1,0 +1,961 @@
+// Host side of liblmdtw_b200.so: device contexts, the level-batched
+// recursion scheduler and the extern "C" ABI declared in include/lmdtw_b200.h.
+//
+// Scheduler (replaces divide._solve, divide.py:148-178).  The reference
+// recurses depth-first, one pivot search at a time.  Here every recursion
+// level is one batch: all internal nodes of the level (of every pair in a
+// batch) launch their forward and reverse half passes as ONE persistent
+// wave_kernel launch, then ONE pivot_kernel launch, then one 48-byte-per-node
+// device->host copy of the pivots.  Leaves (divide.py:153-157) accumulate and
+// are filled + backtraced in one batched launch at the end.  The pivot trace
+// is re-emitted in the reference's pre-order DFS, the path is the in-order
+// concatenation of leaf paths (divide.py:176-178), and the returned cost is
+// the reference's path_cost: per-cell costs summed sequentially in the
+// accumulation dtype (core.py:191-197).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "lmdtw_b200.h"
+#include "lmdtw_internal.h"
+
+using namespace lmdtw;
+
+struct lmdtw_result {
+    lmdtw_align_info_t info;
+    std::vector<int64_t> path;
+    std::vector<lmdtw_pivot_t> pivots;
+};
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+struct Stats {
+    std::mutex mu;
+    double wave_ms = 0, leaf_ms = 0, pivot_ms = 0;
+    long long wave_launches = 0, wave_cells = 0, leaf_cells = 0;
+} g_stats;
+std::atomic<int> g_profile{0};
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* what) {
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation)
+        return set_err(LMDTW_ENOMEM, std::string("device out of memory in ") + what);
+    return set_err(LMDTW_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(x)                                        \
+    do {                                             \
+        cudaError_t _e = (x);                        \
+        if (_e != cudaSuccess) return cuda_err(_e, #x); \
+    } while (0)
+#define TRY(x)                 \
+    do {                       \
+        int _r = (x);          \
+        if (_r != LMDTW_OK) return _r; \
+    } while (0)
+
+struct DBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = std::max<size_t>(n + n / 4, 4096);
+        cudaError_t e = cudaMalloc(&p, c);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            return e;
+        }
+        cap = c;
+        return cudaSuccess;
+    }
+    template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct HBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = std::max<size_t>(n + n / 4, 4096);
+        cudaError_t e = cudaMallocHost(&p, c);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            return e;
+        }
+        cap = c;
+        return cudaSuccess;
+    }
+    template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct Ctx {
+    int device = 0;
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    DBuf xraw, yraw, xp, yp, passes, items, counter, out, bnd, pdesc, pout, ldesc, bp, path, pcost, plen,
+        lcost, tab;
+    HBuf h_passes, h_items, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
+    long long call_launches = 0;
+    long long h2d = 0, d2h = 0;
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<Ctx>> g_ctx;
+
+int get_ctx(int device, Ctx** out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return set_err(LMDTW_ECUDA, "no CUDA device available (liblmdtw_b200 has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return set_err(LMDTW_EINVAL, "bad device index");
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    if ((int)g_ctx.size() < n) g_ctx.resize(n);
+    if (!g_ctx[device]) {
+        std::unique_ptr<Ctx> c(new Ctx());
+        c->device = device;
+        CU(cudaSetDevice(device));
+        CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        CU(cudaEventCreate(&c->ev0));
+        CU(cudaEventCreate(&c->ev1));
+        g_ctx[device] = std::move(c);
+    }
+    *out = g_ctx[device].get();
+    return LMDTW_OK;
+}
+
+inline int64_t dlen(int64_t k, int64_t M, int64_t N) {
+    if (k < 0 || k > M + N - 2) return 0;
+    return std::min(std::min(k, M - 1), std::min(N - 1, M + N - 2 - k)) + 1;
+}
+
+// Number of cells (i,j), i<M, j<N with i+j <= kstop.
+int64_t cells_upto(int64_t kstop, int64_t M, int64_t N) {
+    if (kstop < 0) return 0;
+    const int64_t imax = std::min(M - 1, kstop);
+    int64_t total = 0;
+    // rows with kstop - i + 1 >= N contribute N
+    const int64_t ifull = std::min(imax, kstop - N + 1);
+    int64_t start = 0;
+    if (ifull >= 0) {
+        total += (ifull + 1) * N;
+        start = ifull + 1;
+    }
+    if (start <= imax) {
+        // sum_{i=start}^{imax} (kstop - i + 1)
+        const int64_t a = kstop - start + 1, b = kstop - imax + 1, cnt = imax - start + 1;
+        total += (a + b) * cnt / 2;
+    }
+    return total;
+}
+
+// diagonal.py:160-169: max over k<=kstop of 2*(L(k-2)+L(k-1)+L(k)); the window
+// sum is unimodal with its peak at k in [m, m+2], m = min(M,N)-1.
+int64_t peak_values(int64_t kstop, int64_t M, int64_t N) {
+    auto W = [&](int64_t k) { return dlen(k - 2, M, N) + dlen(k - 1, M, N) + dlen(k, M, N); };
+    const int64_t m = std::min(M, N) - 1;
+    int64_t best = W(kstop);
+    for (int64_t k = m; k <= m + 2; k++)
+        if (k >= 0 && k <= kstop) best = std::max(best, W(k));
+    return 2 * best;
+}
+
+struct Inst {  // divide._Instrument (divide.py:60-94)
+    int64_t cells = 0, budget = 0, next_report = 0, peak_diag = 0, peak_table = 0;
+    lmdtw_progress_fn cb = nullptr;
+    void* user = nullptr;
+    void add(int64_t n) {
+        cells += n;
+        if (cb && cells >= next_report) {
+            next_report = cells + std::max<int64_t>(1, budget / 100);
+            cb(cells, budget, user);
+        }
+    }
+    // A level is one "completed diagonal batch"; report it in <=1% slices.
+    void add_batch(int64_t n) {
+        const int64_t step = std::max<int64_t>(1, budget / 100);
+        while (n > 0) {
+            const int64_t s = std::min(n, step);
+            add(s);
+            n -= s;
+        }
+    }
+};
+
+struct Node {
+    int64_t i_off, j_off, M, N;
+    int pair;
+    int left = -1, right = -1;
+    int64_t pi = -1, pj = -1, k = -1;
+    double total = 0;
+    int leaf = -1;  // index into leaf list
+};
+
+struct Engine {
+    Ctx& c;
+    int prec, d, dp, R, H;
+    size_t esz;
+    int tie[3] = {2, 0, 1};
+    Engine(Ctx& ctx, int precision, int dim) : c(ctx), prec(precision), d(dim) {
+        dp = supported_dp(prec, d);
+        R = rows_per_lane(prec, dp);
+        H = 32 * R;
+        esz = prec == 32 ? 4 : 8;
+    }
+
+    int launched(cudaError_t e, const char* what) {
+        if (e != cudaSuccess) return cuda_err(e, what);
+        c.call_launches++;
+        g_launches++;
+        return LMDTW_OK;
+    }
+
+    // Copy features (host or device float32) into the padded dtype arrays.
+    int stage(const float* const* src, const int64_t* rows, int n, int mem, bool isx, std::vector<int64_t>& base) {
+        int64_t total = 0;
+        base.resize(n);
+        for (int p = 0; p < n; p++) {
+            base[p] = total;
+            total += rows[p];
+        }
+        DBuf& raw = isx ? c.xraw : c.yraw;
+        DBuf& pad = isx ? c.xp : c.yp;
+        CU(pad.ensure((size_t)total * dp * esz));
+        if (mem == LMDTW_MEM_HOST) {
+            CU(raw.ensure((size_t)total * d * sizeof(float)));
+            for (int p = 0; p < n; p++) {
+                CU(cudaMemcpyAsync(raw.as<float>() + base[p] * d, src[p], (size_t)rows[p] * d * sizeof(float),
+                                   cudaMemcpyHostToDevice, c.st));
+                c.h2d += (long long)rows[p] * d * sizeof(float);
+            }
+            TRY(launched(launch_pad_cast(prec, raw.as<float>(), total, d, dp, pad.p, c.st), "pad_cast"));
+        } else {
+            for (int p = 0; p < n; p++) {
+                char* dst = (char*)pad.p + (size_t)base[p] * dp * esz;
+                TRY(launched(launch_pad_cast(prec, src[p], rows[p], d, dp, dst, c.st), "pad_cast"));
+            }
+        }
+        return LMDTW_OK;
+    }
+
+    // Work queue: (pass, strip) ordered by strip length, longest first; ties
+    // by (pass, strip).  Lengths never increase along a pass, so each strip's
+    // predecessor precedes it (the persistent kernel's deadlock freedom).
+    void make_items(const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
+        int64_t total = 0, maxlen = 0;
+        for (const auto& p : P) {
+            total += p.nstrips;
+            maxlen = std::max<int64_t>(maxlen, p.N + 32);
+        }
+        auto len_of = [&](const PassDesc& p, int a) -> int64_t {
+            int64_t je = std::min<int64_t>(p.N - 1, (int64_t)p.kstop - (int64_t)a * H);
+            return je + 32;
+        };
+        std::vector<int64_t> cnt(maxlen + 2, 0);
+        for (size_t q = 0; q < P.size(); q++)
+            for (int a = 0; a < P[q].nstrips; a++) cnt[maxlen - len_of(P[q], a)]++;
+        int64_t acc = 0;
+        for (auto& v : cnt) {
+            int64_t t = v;
+            v = acc;
+            acc += t;
+        }
+        items.assign(total, WorkItem{0, 0});
+        for (size_t q = 0; q < P.size(); q++)
+            for (int a = 0; a < P[q].nstrips; a++) items[cnt[maxlen - len_of(P[q], a)]++] = WorkItem{(int)q, a};
+    }
+
+    int run_wave(const std::vector<PassDesc>& P, int64_t bnd_total, bool leaf, void* tab, void* lcost,
+                 int64_t cells) {
+        std::vector<WorkItem> items;
+        make_items(P, items);
+        CU(c.h_passes.ensure(P.size() * sizeof(PassDesc)));
+        CU(c.h_items.ensure(items.size() * sizeof(WorkItem)));
+        memcpy(c.h_passes.p, P.data(), P.size() * sizeof(PassDesc));
+        memcpy(c.h_items.p, items.data(), items.size() * sizeof(WorkItem));
+        CU(c.passes.ensure(P.size() * sizeof(PassDesc)));
+        CU(c.items.ensure(items.size() * sizeof(WorkItem)));
+        CU(c.counter.ensure(sizeof(int)));
+        CU(c.bnd.ensure((size_t)bnd_total * esz));
+        CU(cudaMemcpyAsync(c.passes.p, c.h_passes.p, P.size() * sizeof(PassDesc), cudaMemcpyHostToDevice, c.st));
+        CU(cudaMemcpyAsync(c.items.p, c.h_items.p, items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice, c.st));
+        CU(cudaMemsetAsync(c.counter.p, 0, sizeof(int), c.st));
+        CU(cudaMemsetAsync(c.bnd.p, 0xFF, (size_t)bnd_total * esz, c.st));
+        WaveLaunch w{};
+        w.X = c.xp.p;
+        w.Y = c.yp.p;
+        w.dp = dp;
+        w.precision = prec;
+        w.passes = c.passes.as<PassDesc>();
+        w.items = c.items.as<WorkItem>();
+        w.nitems = (int)items.size();
+        w.counter = c.counter.as<int>();
+        w.out = c.out.p;
+        w.bnd = c.bnd.p;
+        w.bp = c.bp.as<unsigned long long>();
+        w.tab = tab;
+        w.leaf_cost = lcost;
+        w.tie0 = tie[0];
+        w.tie1 = tie[1];
+        w.tie2 = tie[2];
+        w.leaf = leaf ? 1 : 0;
+        w.grid_warps = 0;
+        const bool prof = g_profile.load() != 0;
+        if (prof) CU(cudaEventRecord(c.ev0, c.st));
+        TRY(launched(launch_wave(w, c.st), leaf ? "leaf wave_kernel" : "wave_kernel"));
+        if (prof) {
+            CU(cudaEventRecord(c.ev1, c.st));
+            CU(cudaEventSynchronize(c.ev1));
+            float ms = 0;
+            CU(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+            std::lock_guard<std::mutex> g(g_stats.mu);
+            if (leaf) {
+                g_stats.leaf_ms += ms;
+                g_stats.leaf_cells += cells;
+            } else {
+                g_stats.wave_ms += ms;
+                g_stats.wave_launches += 1;
+                g_stats.wave_cells += cells;
+            }
+        }
+        return LMDTW_OK;
+    }
+
+    PassDesc half_pass_desc(int64_t x_off, int64_t y_off, int64_t M, int64_t N, int64_t kstop, int rev,
+                            int64_t& out_total, int64_t& bnd_total) {
+        PassDesc p{};
+        p.x_off = x_off;
+        p.y_off = y_off;
+        p.M = (int32_t)M;
+        p.N = (int32_t)N;
+        p.kstop = (int32_t)kstop;
+        p.reverse = rev;
+        p.rows = (int32_t)std::min<int64_t>(M, kstop + 1);
+        p.nstrips = (p.rows + H - 1) / H;
+        for (int s = 0; s < 3; s++) {
+            p.out_off[s] = out_total;
+            out_total += dlen(kstop - 2 + s, M, N);
+        }
+        for (int s = 0; s < 3; s++) {
+            p.out_off[3 + s] = out_total;
+            out_total += dlen(kstop - 2 + s, M, N);
+        }
+        p.bnd_off = bnd_total;
+        bnd_total += 2 * N;
+        p.bp_off = 0;
+        p.tab_off = -1;
+        p.w64 = 0;
+        p.leaf_id = -1;
+        return p;
+    }
+
+    // Batched find_pivot over `nodes` (indices into `all`).
+    int pivot_level(std::vector<Node>& all, const std::vector<int>& nodes, const std::vector<int64_t>& xb,
+                    const std::vector<int64_t>& yb, std::vector<int64_t>* cells_out,
+                    std::vector<int64_t>* peak_out, int highest) {
+        std::vector<PassDesc> P;
+        std::vector<PivotDesc> V;
+        int64_t out_total = 0, bnd_total = 0, cells = 0;
+        P.reserve(nodes.size() * 2);
+        for (int q : nodes) {
+            const Node& n = all[q];
+            const int64_t K = n.M + n.N - 1;
+            const int64_t kf = (K + 1) / 2;
+            const int64_t kb = (K % 2 == 0) ? kf + 1 : kf;
+            PivotDesc v{};
+            v.fwd = (int)P.size();
+            P.push_back(half_pass_desc(xb[n.pair] + n.i_off, yb[n.pair] + n.j_off, n.M, n.N, kf, 0, out_total,
+                                       bnd_total));
+            v.bwd = (int)P.size();
+            P.push_back(half_pass_desc(xb[n.pair] + n.i_off, yb[n.pair] + n.j_off, n.M, n.N, kb, 1, out_total,
+                                       bnd_total));
+            v.M = (int)n.M;
+            v.N = (int)n.N;
+            v.kf = (int)kf;
+            v.kb = (int)kb;
+            v.highest = highest;
+            V.push_back(v);
+            const int64_t cl = cells_upto(kf, n.M, n.N) + cells_upto(kb, n.M, n.N);
+            cells += cl;
+            if (cells_out) cells_out->push_back(cl);
+            if (peak_out)
+                peak_out->push_back(std::max(peak_values(kf, n.M, n.N), peak_values(kb, n.M, n.N)));
+        }
+        CU(c.out.ensure((size_t)out_total * esz));
+        TRY(run_wave(P, bnd_total, false, nullptr, nullptr, cells));
+        CU(c.pdesc.ensure(V.size() * sizeof(PivotDesc)));
+        CU(c.pout.ensure(V.size() * sizeof(PivotOut)));
+        CU(c.h_pdesc.ensure(V.size() * sizeof(PivotDesc)));
+        CU(c.h_pout.ensure(V.size() * sizeof(PivotOut)));
+        memcpy(c.h_pdesc.p, V.data(), V.size() * sizeof(PivotDesc));
+        CU(cudaMemcpyAsync(c.pdesc.p, c.h_pdesc.p, V.size() * sizeof(PivotDesc), cudaMemcpyHostToDevice, c.st));
+        TRY(launched(launch_pivots(prec, c.passes.as<PassDesc>(), c.pdesc.as<PivotDesc>(), (int)V.size(), c.out.p,
+                                   c.pout.as<PivotOut>(), c.st),
+                     "pivot_kernel"));
+        CU(cudaMemcpyAsync(c.h_pout.p, c.pout.p, V.size() * sizeof(PivotOut), cudaMemcpyDeviceToHost, c.st));
+        c.d2h += V.size() * sizeof(PivotOut);
+        CU(cudaStreamSynchronize(c.st));
+        const PivotOut* po = c.h_pout.as<PivotOut>();
+        for (size_t q = 0; q < nodes.size(); q++) {
+            Node& n = all[nodes[q]];
+            n.pi = po[q].i;
+            n.pj = po[q].j;
+            n.k = po[q].k;
+            n.total = po[q].total;
+        }
+        return LMDTW_OK;
+    }
+
+    // Batched dtw_full over leaf nodes.  Fills per-leaf reversed paths (local
+    // coordinates), per-cell costs, lengths, and D[M-1,N-1].
+    int leaves(const std::vector<Node>& all, const std::vector<int>& leafs, const std::vector<int64_t>& xb,
+               const std::vector<int64_t>& yb, void* tab_host, std::vector<int64_t>& path_off,
+               std::vector<int>& plen) {
+        const int n = (int)leafs.size();
+        std::vector<PassDesc> P(n);
+        std::vector<LeafDesc> L(n);
+        int64_t bnd_total = 0, bp_total = 0, path_total = 0, cells = 0;
+        path_off.resize(n);
+        for (int q = 0; q < n; q++) {
+            const Node& nd = all[leafs[q]];
+            PassDesc& p = P[q];
+            p = PassDesc{};
+            p.x_off = xb[nd.pair] + nd.i_off;
+            p.y_off = yb[nd.pair] + nd.j_off;
+            p.M = (int32_t)nd.M;
+            p.N = (int32_t)nd.N;
+            p.kstop = (int32_t)(nd.M + nd.N - 2);
+            p.reverse = 0;
+            p.rows = (int32_t)nd.M;
+            p.nstrips = (p.rows + H - 1) / H;
+            p.bnd_off = bnd_total;
+            bnd_total += 2 * nd.N;
+            p.w64 = (int32_t)((nd.N + 31) / 32);
+            p.bp_off = bp_total;
+            bp_total += nd.M * p.w64;
+            p.tab_off = tab_host ? 0 : -1;
+            p.leaf_id = q;
+            LeafDesc& l = L[q];
+            l = LeafDesc{};
+            l.x_off = p.x_off;
+            l.y_off = p.y_off;
+            l.M = p.M;
+            l.N = p.N;
+            l.pass = q;
+            l.path_off = path_total;
+            l.bp_off = p.bp_off;
+            l.w64 = p.w64;
+            path_off[q] = path_total;
+            path_total += nd.M + nd.N - 1;
+            cells += nd.M * nd.N;
+        }
+        CU(c.bp.ensure((size_t)std::max<int64_t>(bp_total, 1) * 8));
+        CU(c.lcost.ensure((size_t)n * esz));
+        void* tab_dev = nullptr;
+        if (tab_host) {
+            CU(c.tab.ensure((size_t)all[leafs[0]].M * all[leafs[0]].N * esz));
+            tab_dev = c.tab.p;
+        }
+        TRY(run_wave(P, bnd_total, true, tab_dev, c.lcost.p, cells));
+        CU(c.ldesc.ensure(n * sizeof(LeafDesc)));
+        CU(cudaMemcpyAsync(c.ldesc.p, L.data(), n * sizeof(LeafDesc), cudaMemcpyHostToDevice, c.st));
+        CU(c.path.ensure((size_t)path_total * 2 * sizeof(int)));
+        CU(c.pcost.ensure((size_t)path_total * esz));
+        CU(c.plen.ensure((size_t)n * sizeof(int)));
+        TRY(launched(launch_backtrace(prec, dp, c.xp.p, c.yp.p, c.ldesc.as<LeafDesc>(), n,
+                                      c.bp.as<unsigned long long>(), c.path.as<int>(), c.pcost.p, c.plen.as<int>(),
+                                      c.st),
+                     "backtrace_kernel"));
+        CU(c.h_path.ensure((size_t)path_total * 2 * sizeof(int)));
+        CU(c.h_pcost.ensure((size_t)path_total * esz));
+        CU(c.h_plen.ensure((size_t)n * sizeof(int)));
+        CU(c.h_lcost.ensure((size_t)n * esz));
+        CU(cudaMemcpyAsync(c.h_path.p, c.path.p, (size_t)path_total * 2 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        CU(cudaMemcpyAsync(c.h_pcost.p, c.pcost.p, (size_t)path_total * esz, cudaMemcpyDeviceToHost, c.st));
+        CU(cudaMemcpyAsync(c.h_plen.p, c.plen.p, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        CU(cudaMemcpyAsync(c.h_lcost.p, c.lcost.p, (size_t)n * esz, cudaMemcpyDeviceToHost, c.st));
+        c.d2h += (long long)path_total * (2 * sizeof(int) + esz) + n * (sizeof(int) + esz);
+        if (tab_host) {
+            const size_t tb = (size_t)all[leafs[0]].M * all[leafs[0]].N * esz;
+            CU(cudaMemcpyAsync(tab_host, tab_dev, tb, cudaMemcpyDeviceToHost, c.st));
+            c.d2h += tb;
+        }
+        CU(cudaStreamSynchronize(c.st));
+        plen.assign(c.h_plen.as<int>(), c.h_plen.as<int>() + n);
+        for (int q = 0; q < n; q++)
+            if (plen[q] < 0) {
+                const Node& nd = all[leafs[q]];
+                char buf[160];
+                snprintf(buf, sizeof buf, "backtrace hit SELF before (0, 0) in %lldx%lld leaf",
+                         (long long)nd.M, (long long)nd.N);
+                return set_err(LMDTW_EINTERNAL, buf);
+            }
+        return LMDTW_OK;
+    }
+
+    double leaf_cost(int q) const {
+        return prec == 32 ? (double)c.h_lcost.as<float>()[q] : c.h_lcost.as<double>()[q];
+    }
+};
+
+template <typename T> double seq_sum(const std::vector<const T*>& parts, const std::vector<int>& lens) {
+    T total = T(0);
+    for (size_t p = 0; p < parts.size(); p++)
+        for (int q = 0; q < lens[p]; q++) total = total + parts[p][q];
+    return (double)total;
+}
+
+int validate_common(int64_t M, int64_t N, int d, int prec) {
+    if (M < 1 || N < 1) return set_err(LMDTW_EINVAL, "series must have length >= 1");
+    if (d < 1) return set_err(LMDTW_EINVAL, "feature dimension must be >= 1");
+    if (prec != 32 && prec != 64) return set_err(LMDTW_EINVAL, "precision must be 32 or 64");
+    if (supported_dp(prec, d) < 0) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "feature dimension %d exceeds the kernels' maximum (%d) for precision %d", d,
+                 lmdtw_max_dim(prec), prec);
+        return set_err(LMDTW_EINVAL, buf);
+    }
+    if (M + N > (int64_t)1 << 30) return set_err(LMDTW_EINVAL, "M + N too large (limit 2^30)");
+    return LMDTW_OK;
+}
+
+int validate_tie(const int32_t* tie) {
+    int seen = 0;
+    for (int q = 0; q < 3; q++) {
+        if (tie[q] < 0 || tie[q] > 2) return set_err(LMDTW_EINVAL, "tie codes must be a permutation of 0,1,2");
+        seen |= 1 << tie[q];
+    }
+    if (seen != 7) return set_err(LMDTW_EINVAL, "tie codes must be a permutation of 0,1,2");
+    return LMDTW_OK;
+}
+
+// Core of lmdtw_align / lmdtw_align_batch.
+int align_core(int device, int npairs, const float* const* X, const int64_t* M, const float* const* Y,
+               const int64_t* N, int d, const lmdtw_config_t& cfg, int mem, lmdtw_progress_fn progress, void* user,
+               std::vector<lmdtw_result*>& results) {
+    if (npairs < 1) return set_err(LMDTW_EINVAL, "npairs must be >= 1");
+    for (int p = 0; p < npairs; p++) TRY(validate_common(M[p], N[p], d, cfg.precision));
+    if (cfg.min_dim < 2) return set_err(LMDTW_EINVAL, "min_dim must be >= 2");
+    TRY(validate_tie(cfg.tie));
+    if (cfg.pivot_highest != 0 && cfg.pivot_highest != 1) return set_err(LMDTW_EINVAL, "unknown pivot_tie_rule");
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    c->call_launches = 0;
+    c->h2d = c->d2h = 0;
+    Engine E(*c, cfg.precision, d);
+    E.tie[0] = cfg.tie[0];
+    E.tie[1] = cfg.tie[1];
+    E.tie[2] = cfg.tie[2];
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(X, M, npairs, mem, true, xb));
+    TRY(E.stage(Y, N, npairs, mem, false, yb));
+
+    std::vector<Inst> inst(npairs);
+    std::vector<Node> nodes;
+    std::vector<int> level;
+    for (int p = 0; p < npairs; p++) {
+        inst[p].budget = 2 * M[p] * N[p];
+        inst[p].cb = (npairs == 1) ? progress : nullptr;
+        inst[p].user = user;
+        Node n;
+        n.i_off = 0;
+        n.j_off = 0;
+        n.M = M[p];
+        n.N = N[p];
+        n.pair = p;
+        nodes.push_back(n);
+        level.push_back((int)nodes.size() - 1);
+    }
+    std::vector<int> leafs;
+    int64_t nlevels = 0;
+    while (!level.empty()) {
+        std::vector<int> internal;
+        for (int q : level) {
+            const Node& n = nodes[q];
+            if (n.M < cfg.min_dim || n.N < cfg.min_dim || n.M + n.N <= 5) {
+                nodes[q].leaf = (int)leafs.size();
+                leafs.push_back(q);
+            } else {
+                internal.push_back(q);
+            }
+        }
+        if (internal.empty()) break;
+        nlevels++;
+        std::vector<int64_t> cells, peaks;
+        TRY(E.pivot_level(nodes, internal, xb, yb, &cells, &peaks, cfg.pivot_highest));
+        std::vector<int> next;
+        for (size_t q = 0; q < internal.size(); q++) {
+            const int id = internal[q];
+            Node parent = nodes[id];
+            Inst& in = inst[parent.pair];
+            in.peak_diag = std::max(in.peak_diag, peaks[q]);
+            in.add_batch(cells[q]);
+            Node l, r;
+            l.i_off = parent.i_off;
+            l.j_off = parent.j_off;
+            l.M = parent.pi + 1;
+            l.N = parent.pj + 1;
+            l.pair = parent.pair;
+            r.i_off = parent.i_off + parent.pi;
+            r.j_off = parent.j_off + parent.pj;
+            r.M = parent.M - parent.pi;
+            r.N = parent.N - parent.pj;
+            r.pair = parent.pair;
+            nodes.push_back(l);
+            nodes[id].left = (int)nodes.size() - 1;
+            next.push_back(nodes[id].left);
+            nodes.push_back(r);
+            nodes[id].right = (int)nodes.size() - 1;
+            next.push_back(nodes[id].right);
+        }
+        level.swap(next);
+    }
+    // leaves, in node order (the stitching below walks the tree)
+    std::vector<int64_t> poff;
+    std::vector<int> plen;
+    TRY(E.leaves(nodes, leafs, xb, yb, nullptr, poff, plen));
+
+    const int* hpath = c->h_path.as<int>();
+    results.assign(npairs, nullptr);
+    for (int p = 0; p < npairs; p++) {
+        std::unique_ptr<lmdtw_result> res(new lmdtw_result());
+        Inst& in = inst[p];
+        // pre-order DFS: pivots and leaf sequence
+        std::vector<int> stack{p};  // root node index == p
+        std::vector<int> leaf_seq;
+        while (!stack.empty()) {
+            const int id = stack.back();
+            stack.pop_back();
+            const Node& n = nodes[id];
+            if (n.leaf >= 0) {
+                leaf_seq.push_back(n.leaf);
+                const int64_t cl = n.M * n.N;
+                in.add_batch(cl);
+                in.peak_table = std::max(in.peak_table, cl);
+                continue;
+            }
+            lmdtw_pivot_t pv;
+            pv.i = n.i_off + n.pi;
+            pv.j = n.j_off + n.pj;
+            pv.i_off = n.i_off;
+            pv.j_off = n.j_off;
+            pv.M = n.M;
+            pv.N = n.N;
+            pv.sub_i = n.pi;
+            pv.sub_j = n.pj;
+            pv.diagonal_k = n.k;
+            pv.total_at_pivot = n.total;
+            res->pivots.push_back(pv);
+            stack.push_back(n.right);
+            stack.push_back(n.left);
+        }
+        // path: leaf paths in order, first cell of every later leaf dropped
+        std::vector<const void*> cparts;
+        std::vector<int> clens;
+        int64_t K = 0;
+        for (size_t s = 0; s < leaf_seq.size(); s++) K += plen[leaf_seq[s]] - (s ? 1 : 0);
+        res->path.resize(2 * K);
+        int64_t w = 0;
+        std::vector<const float*> cf;
+        std::vector<const double*> cd;
+        for (size_t s = 0; s < leaf_seq.size(); s++) {
+            const int lf = leaf_seq[s];
+            const Node& n = nodes[leafs[lf]];
+            const int len = plen[lf];
+            const int* lp = hpath + 2 * poff[lf];  // reversed: lp[0] is the corner
+            const int skip = s ? 1 : 0;
+            for (int q = len - 1 - skip; q >= 0; q--) {
+                res->path[2 * w] = n.i_off + lp[2 * q];
+                res->path[2 * w + 1] = n.j_off + lp[2 * q + 1];
+                w++;
+            }
+        }
+        // cost: sequential sum over the path in order (core.py:191-197)
+        if (cfg.precision == 32) {
+            const float* pc = c->h_pcost.as<float>();
+            float total = 0.0f;
+            for (size_t s = 0; s < leaf_seq.size(); s++) {
+                const int lf = leaf_seq[s];
+                for (int q = plen[lf] - 1 - (s ? 1 : 0); q >= 0; q--) total = total + pc[poff[lf] + q];
+            }
+            res->info.cost = (double)total;
+        } else {
+            const double* pc = c->h_pcost.as<double>();
+            double total = 0.0;
+            for (size_t s = 0; s < leaf_seq.size(); s++) {
+                const int lf = leaf_seq[s];
+                for (int q = plen[lf] - 1 - (s ? 1 : 0); q >= 0; q--) total = total + pc[poff[lf] + q];
+            }
+            res->info.cost = total;
+        }
+        if (in.cb) in.cb(in.cells, in.budget, in.user);
+        res->info.path_len = K;
+        res->info.cells_processed = in.cells;
+        res->info.cells_budget = in.budget;
+        res->info.peak_diag_values = in.peak_diag;
+        res->info.peak_table_cells = in.peak_table;
+        res->info.n_pivots = (int64_t)res->pivots.size();
+        res->info.n_levels = nlevels;
+        res->info.gpu_launches = c->call_launches;
+        res->info.h2d_bytes = c->h2d;
+        res->info.d2h_bytes = c->d2h;
+        results[p] = res.release();
+    }
+    return LMDTW_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* lmdtw_version(void) { return "lmdtw_b200 0.1.0 (sm_100a)"; }
+const char* lmdtw_last_error(void) { return g_err.c_str(); }
+
+int lmdtw_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int lmdtw_max_dim(int32_t precision) { return precision == 32 ? 64 : 48; }
+
+int64_t lmdtw_diag_length(int64_t k, int64_t M, int64_t N) { return dlen(k, M, N); }
+int64_t lmdtw_cells_upto(int64_t kstop, int64_t M, int64_t N) { return cells_upto(kstop, M, N); }
+int64_t lmdtw_peak_retained_values(int64_t kstop, int64_t M, int64_t N) { return peak_values(kstop, M, N); }
+int64_t lmdtw_launch_count(void) { return g_launches.load(); }
+
+void lmdtw_profile_enable(int on) { g_profile.store(on ? 1 : 0); }
+void lmdtw_profile_reset(void) {
+    std::lock_guard<std::mutex> g(g_stats.mu);
+    g_stats.wave_ms = g_stats.leaf_ms = g_stats.pivot_ms = 0;
+    g_stats.wave_launches = g_stats.wave_cells = g_stats.leaf_cells = 0;
+}
+// out[0]=wave_ms out[1]=wave_launches out[2]=wave_cells out[3]=leaf_ms out[4]=leaf_cells
+void lmdtw_profile_get(double* out) {
+    std::lock_guard<std::mutex> g(g_stats.mu);
+    out[0] = g_stats.wave_ms;
+    out[1] = (double)g_stats.wave_launches;
+    out[2] = (double)g_stats.wave_cells;
+    out[3] = g_stats.leaf_ms;
+    out[4] = (double)g_stats.leaf_cells;
+}
+// The stream every kernel of `device` is launched on (for event timing).
+void* lmdtw_stream(int device) {
+    Ctx* c = nullptr;
+    if (get_ctx(device, &c) != LMDTW_OK) return nullptr;
+    return (void*)c->st;
+}
+
+int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d, int64_t kstop,
+                    int32_t reverse, int32_t precision, int32_t mem, void* out_d[3], void* out_c[3],
+                    int64_t* cells) {
+    TRY(validate_common(M, N, d, precision));
+    if (kstop < 2 || kstop > M + N - 2) return set_err(LMDTW_EINVAL, "kstop out of range [2, M+N-2]");
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    c->call_launches = 0;
+    Engine E(*c, precision, d);
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&X, &M, 1, mem, true, xb));
+    TRY(E.stage(&Y, &N, 1, mem, false, yb));
+    int64_t out_total = 0, bnd_total = 0;
+    std::vector<PassDesc> P{E.half_pass_desc(0, 0, M, N, kstop, reverse ? 1 : 0, out_total, bnd_total)};
+    CU(c->out.ensure((size_t)out_total * E.esz));
+    const int64_t cl = cells_upto(kstop, M, N);
+    TRY(E.run_wave(P, bnd_total, false, nullptr, nullptr, cl));
+    for (int s = 0; s < 3; s++) {
+        const int64_t L = dlen(kstop - 2 + s, M, N);
+        if (L > 0 && out_d && out_d[s])
+            CU(cudaMemcpyAsync(out_d[s], (char*)c->out.p + P[0].out_off[s] * E.esz, L * E.esz,
+                               cudaMemcpyDeviceToHost, c->st));
+        if (L > 0 && out_c && out_c[s])
+            CU(cudaMemcpyAsync(out_c[s], (char*)c->out.p + P[0].out_off[3 + s] * E.esz, L * E.esz,
+                               cudaMemcpyDeviceToHost, c->st));
+    }
+    CU(cudaStreamSynchronize(c->st));
+    if (cells) *cells = cl;
+    return LMDTW_OK;
+}
+
+int lmdtw_find_pivot(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d,
+                     int32_t precision, int32_t pivot_highest, int32_t mem, int64_t* i, int64_t* j,
+                     int64_t* diagonal_k, double* total, int64_t* cells, int64_t* peak) {
+    TRY(validate_common(M, N, d, precision));
+    if (M + N - 2 < 2) return set_err(LMDTW_EINVAL, "too small for a pivot search; use dtw_full");
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    c->call_launches = 0;
+    Engine E(*c, precision, d);
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&X, &M, 1, mem, true, xb));
+    TRY(E.stage(&Y, &N, 1, mem, false, yb));
+    std::vector<Node> nodes(1);
+    nodes[0].i_off = 0;
+    nodes[0].j_off = 0;
+    nodes[0].M = M;
+    nodes[0].N = N;
+    nodes[0].pair = 0;
+    std::vector<int64_t> cl, pk;
+    TRY(E.pivot_level(nodes, std::vector<int>{0}, xb, yb, &cl, &pk, pivot_highest ? 1 : 0));
+    if (i) *i = nodes[0].pi;
+    if (j) *j = nodes[0].pj;
+    if (diagonal_k) *diagonal_k = nodes[0].k;
+    if (total) *total = nodes[0].total;
+    if (cells) *cells = cl[0];
+    if (peak) *peak = pk[0];
+    return LMDTW_OK;
+}
+
+int lmdtw_dtw_full(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d,
+                   const int32_t tie[3], int32_t precision, int32_t mem, double* cost, int64_t* path_out,
+                   int64_t* path_len, void* D_out) {
+    TRY(validate_common(M, N, d, precision));
+    TRY(validate_tie(tie));
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    c->call_launches = 0;
+    Engine E(*c, precision, d);
+    E.tie[0] = tie[0];
+    E.tie[1] = tie[1];
+    E.tie[2] = tie[2];
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&X, &M, 1, mem, true, xb));
+    TRY(E.stage(&Y, &N, 1, mem, false, yb));
+    std::vector<Node> nodes(1);
+    nodes[0].i_off = 0;
+    nodes[0].j_off = 0;
+    nodes[0].M = M;
+    nodes[0].N = N;
+    nodes[0].pair = 0;
+    std::vector<int64_t> poff;
+    std::vector<int> plen;
+    TRY(E.leaves(nodes, std::vector<int>{0}, xb, yb, D_out, poff, plen));
+    const int* lp = c->h_path.as<int>();
+    const int len = plen[0];
+    for (int q = 0; q < len; q++) {
+        path_out[2 * q] = lp[2 * (len - 1 - q)];
+        path_out[2 * q + 1] = lp[2 * (len - 1 - q) + 1];
+    }
+    if (path_len) *path_len = len;
+    if (cost) *cost = E.leaf_cost(0);
+    return LMDTW_OK;
+}
+
+int lmdtw_align(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d,
+                const lmdtw_config_t* cfg, int32_t mem, lmdtw_progress_fn progress, void* user,
+                lmdtw_result_t** result) {
+    if (!cfg || !result) return set_err(LMDTW_EINVAL, "null config/result");
+    std::vector<lmdtw_result*> res;
+    TRY(align_core(device, 1, &X, &M, &Y, &N, d, *cfg, mem, progress, user, res));
+    *result = res[0];
+    return LMDTW_OK;
+}
+
+int lmdtw_align_batch(int device, int32_t npairs, const float* const* X, const int64_t* M, const float* const* Y,
+                      const int64_t* N, int32_t d, const lmdtw_config_t* cfg, int32_t mem,
+                      lmdtw_result_t** results) {
+    if (!cfg || !results) return set_err(LMDTW_EINVAL, "null config/results");
+    std::vector<lmdtw_result*> res;
+    TRY(align_core(device, npairs, X, M, Y, N, d, *cfg, mem, nullptr, nullptr, res));
+    for (int p = 0; p < npairs; p++) results[p] = res[p];
+    return LMDTW_OK;
+}
+
+int lmdtw_result_info(const lmdtw_result_t* r, lmdtw_align_info_t* info) {
+    if (!r || !info) return set_err(LMDTW_EINVAL, "null result");
+    *info = r->info;
+    return LMDTW_OK;
+}
+
+int lmdtw_result_path(const lmdtw_result_t* r, int64_t* path_out) {
+    if (!r || !path_out) return set_err(LMDTW_EINVAL, "null result");
+    memcpy(path_out, r->path.data(), r->path.size() * sizeof(int64_t));
+    return LMDTW_OK;
+}
+
+int lmdtw_result_pivots(const lmdtw_result_t* r, lmdtw_pivot_t* pivots_out) {
+    if (!r || (!pivots_out && !r->pivots.empty())) return set_err(LMDTW_EINVAL, "null result");
+    if (!r->pivots.empty()) memcpy(pivots_out, r->pivots.data(), r->pivots.size() * sizeof(lmdtw_pivot_t));
+    return LMDTW_OK;
+}
+
+void lmdtw_result_free(lmdtw_result_t* r) { delete r; }
+
+int lmdtw_path_cost(const float* X, int64_t M, const float* Y, int64_t N, int32_t d, const int64_t* path,
+                    int64_t K, int32_t precision, double* cost) {
+    if (precision != 32 && precision != 64) return set_err(LMDTW_EINVAL, "precision must be 32 or 64");
+    if (d < 1 || K < 1) return set_err(LMDTW_EINVAL, "empty path or bad dimension");
+    for (int64_t q = 0; q < K; q++)
+        if (path[2 * q] < 0 || path[2 * q] >= M || path[2 * q + 1] < 0 || path[2 * q + 1] >= N)
+            return set_err(LMDTW_EINVAL, "path index out of range");
+    if (precision == 32) {
+        float total = 0.0f;
+        for (int64_t q = 0; q < K; q++) {
+            const float* x = X + path[2 * q] * d;
+            const float* y = Y + path[2 * q + 1] * d;
+            float s = 0.0f;
+            for (int t = 0; t < d; t++) {
+                const float df = x[t] - y[t];
+                const float sq = df * df;
+                s = s + sq;
+            }
+            total = total + std::sqrt(s);
+        }
+        *cost = (double)total;
+    } else {
+        double total = 0.0;
+        for (int64_t q = 0; q < K; q++) {
+            const float* x = X + path[2 * q] * d;
+            const float* y = Y + path[2 * q + 1] * d;
+            double s = 0.0;
+            for (int t = 0; t < d; t++) {
+                const double df = (double)x[t] - (double)y[t];
+                const double sq = df * df;
+                s = s + sq;
+            }
+            total = total + std::sqrt(s);
+        }
+        *cost = total;
+    }
+    return LMDTW_OK;
+}
+
+}  // extern "C"

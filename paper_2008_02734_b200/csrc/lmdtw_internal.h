@@ -1,0 +1,94 @@
+// Internal structures shared by the host scheduler and the sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lmdtw {
+
+// Threads per strip-lane: a warp owns a strip of 32*R grid rows.
+constexpr int kWarp = 32;
+// Steps of boundary prefetch (lane 31 feeds lane 0 of the next strip).
+constexpr int kFeedAhead = 8;
+
+// One DP domain handled by the strip engine.  For a half pass it is the
+// triangle {i + j <= kstop} of an M x N grid (optionally on the reversed
+// series); for a leaf it is the whole grid plus 2-bit backpointers.
+struct PassDesc {
+    int64_t x_off, y_off;   // first row of the sub-block in the padded X / Y arrays
+    int32_t M, N;           // sub-block shape
+    int32_t kstop;          // last anti-diagonal (M+N-2 for leaves)
+    int32_t reverse;        // 1: rows/cols indexed from the end (diag_dtw "reverse")
+    int32_t rows;           // rows taking part: min(M, kstop+1)
+    int32_t nstrips;        // ceil(rows / (32 R))
+    int64_t out_off[6];     // half pass: D(k-2),D(k-1),D(k),C(k-2),C(k-1),C(k)
+    int64_t bnd_off;        // 2 * N boundary slots (double-buffered strip handoff)
+    int64_t bp_off;         // leaf: backpointer words (uint64, 32 cells each)
+    int64_t tab_off;        // leaf: optional full D table (-1 = none)
+    int32_t w64;            // leaf: words per backpointer row = ceil(N/32)
+    int32_t leaf_id;        // leaf: index into per-leaf outputs
+};
+
+struct WorkItem {
+    int32_t pass;
+    int32_t strip;
+};
+
+// Pivot search input: the two passes of one internal node.
+struct PivotDesc {
+    int32_t fwd, bwd;       // PassDesc indices
+    int32_t M, N;
+    int32_t kf, kb;         // kstop of forward / reverse pass
+    int32_t highest;
+    int32_t pad;
+};
+
+struct PivotOut {
+    int64_t i, j, k;
+    double total;
+};
+
+// Leaf backtrace input/output.
+struct LeafDesc {
+    int64_t x_off, y_off;
+    int32_t M, N;
+    int32_t pass;           // PassDesc index of the fill
+    int32_t pad;
+    int64_t path_off;       // capacity M+N-1 (i,j) int32 pairs, written reversed
+    int64_t bp_off;
+    int32_t w64;
+    int32_t pad2;
+};
+
+// Kernel launchers (kernels.cu).  All are asynchronous on `stream`.
+struct WaveLaunch {
+    const void* X;          // padded features, dtype T, row stride dp
+    const void* Y;
+    int dp;                 // padded dimension (template value)
+    int precision;          // 32 / 64
+    const PassDesc* passes;
+    const WorkItem* items;
+    int nitems;
+    int* counter;           // work queue head (zeroed by caller)
+    void* out;              // half-pass diagonal outputs
+    void* bnd;              // strip boundary slots (memset 0xFF by caller)
+    unsigned long long* bp; // leaf backpointers
+    void* tab;              // leaf full tables (may be null)
+    void* leaf_cost;        // leaf D[M-1,N-1], one per leaf_id (may be null)
+    int tie0, tie1, tie2;
+    int leaf;               // 0 half pass, 1 leaf fill
+    int grid_warps;         // persistent warps to launch (0 = auto)
+};
+
+int rows_per_lane(int precision, int dp);
+int supported_dp(int precision, int d);  // padded dim for d, or -1
+cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
+cudaError_t launch_pivots(int precision, const PassDesc* passes, const PivotDesc* piv, int npiv,
+                          const void* out, PivotOut* res, cudaStream_t stream);
+cudaError_t launch_backtrace(int precision, int dp, const void* X, const void* Y, const LeafDesc* leaves,
+                             int nleaves, const unsigned long long* bp, int* path, void* pcost,
+                             int* plen, cudaStream_t stream);
+cudaError_t launch_pad_cast(int precision, const float* src, int64_t rows, int d, int dp, void* dst,
+                            cudaStream_t stream);
+int max_resident_warps(int precision, int dp, int leaf, int device);
+
+}  // namespace lmdtw
