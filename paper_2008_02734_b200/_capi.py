@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblmdtw_b200.so")
+LIB_PATH = os.environ.get("LMDTW_LIB_PATH") or os.path.join(_HERE, "liblmdtw_b200.so")
 
 OK, EINVAL, ENOMEM, ECUDA, EINTERNAL = 0, -1, -2, -3, -4
 MEM_HOST, MEM_DEVICE = 0, 1

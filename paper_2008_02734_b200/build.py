@@ -22,8 +22,9 @@ HEADERS = [os.path.join(CSRC, "lmdtw_internal.h"), os.path.join(INCLUDE, "lmdtw_
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-# -ffp-contract=off on the host side: path_cost must never fuse mul+add.
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+# -fmad=false: ptxas otherwise fuses mul.rn.f32x2 + add.rn.f32x2 into FFMA2,
+# breaking bit parity; -ffp-contract=off: same rule for host-side path_cost.
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-Xptxas", "-warn-spills", "-I", CSRC, "-I", INCLUDE]
 
 

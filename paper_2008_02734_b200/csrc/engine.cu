@@ -229,6 +229,9 @@ struct Engine {
         esz = prec == 32 ? 4 : 8;
     }
 
+    // 64-bit words per boundary element (tagged handoff, see kernels.cu)
+    int64_t bwords() const { return prec == 32 ? 1 : 2; }
+
     int launched(cudaError_t e, const char* what) {
         if (e != cudaSuccess) return cuda_err(e, what);
         c.call_launches++;
@@ -246,7 +249,13 @@ struct Engine {
         }
         DBuf& raw = isx ? c.xraw : c.yraw;
         DBuf& pad = isx ? c.xp : c.yp;
-        CU(pad.ensure((size_t)total * dp * esz));
+        // kPadRows zero rows before and after (see kernels.cu); row r of the
+        // concatenated series lives at padded row kPadRows + r.
+        const size_t rowb = (size_t)dp * esz;
+        CU(pad.ensure((size_t)(total + 2 * kPadRows) * rowb));
+        CU(cudaMemsetAsync(pad.p, 0, kPadRows * rowb, c.st));
+        CU(cudaMemsetAsync((char*)pad.p + (kPadRows + total) * rowb, 0, kPadRows * rowb, c.st));
+        char* body = (char*)pad.p + kPadRows * rowb;
         if (mem == LMDTW_MEM_HOST) {
             CU(raw.ensure((size_t)total * d * sizeof(float)));
             for (int p = 0; p < n; p++) {
@@ -254,13 +263,14 @@ struct Engine {
                                    cudaMemcpyHostToDevice, c.st));
                 c.h2d += (long long)rows[p] * d * sizeof(float);
             }
-            TRY(launched(launch_pad_cast(prec, raw.as<float>(), total, d, dp, pad.p, c.st), "pad_cast"));
+            TRY(launched(launch_pad_cast(prec, raw.as<float>(), total, d, dp, body, c.st), "pad_cast"));
         } else {
             for (int p = 0; p < n; p++) {
-                char* dst = (char*)pad.p + (size_t)base[p] * dp * esz;
+                char* dst = body + (size_t)base[p] * rowb;
                 TRY(launched(launch_pad_cast(prec, src[p], rows[p], d, dp, dst, c.st), "pad_cast"));
             }
         }
+        for (int p = 0; p < n; p++) base[p] += kPadRows;
         return LMDTW_OK;
     }
 
@@ -302,11 +312,11 @@ struct Engine {
         CU(c.passes.ensure(P.size() * sizeof(PassDesc)));
         CU(c.items.ensure(items.size() * sizeof(WorkItem)));
         CU(c.counter.ensure(sizeof(int)));
-        CU(c.bnd.ensure((size_t)bnd_total * esz));
+        CU(c.bnd.ensure((size_t)bnd_total * 8));
         CU(cudaMemcpyAsync(c.passes.p, c.h_passes.p, P.size() * sizeof(PassDesc), cudaMemcpyHostToDevice, c.st));
         CU(cudaMemcpyAsync(c.items.p, c.h_items.p, items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice, c.st));
         CU(cudaMemsetAsync(c.counter.p, 0, sizeof(int), c.st));
-        CU(cudaMemsetAsync(c.bnd.p, 0xFF, (size_t)bnd_total * esz, c.st));
+        CU(cudaMemsetAsync(c.bnd.p, 0xFF, (size_t)bnd_total * 8, c.st));  // tag -1
         WaveLaunch w{};
         w.X = c.xp.p;
         w.Y = c.yp.p;
@@ -367,7 +377,7 @@ struct Engine {
             out_total += dlen(kstop - 2 + s, M, N);
         }
         p.bnd_off = bnd_total;
-        bnd_total += 2 * N;
+        bnd_total += 2 * N * bwords();
         p.bp_off = 0;
         p.tab_off = -1;
         p.w64 = 0;
@@ -455,7 +465,7 @@ struct Engine {
             p.rows = (int32_t)nd.M;
             p.nstrips = (p.rows + H - 1) / H;
             p.bnd_off = bnd_total;
-            bnd_total += 2 * nd.N;
+            bnd_total += 2 * nd.N * bwords();
             p.w64 = (int32_t)((nd.N + 31) / 32);
             p.bp_off = bp_total;
             bp_total += nd.M * p.w64;
@@ -776,6 +786,52 @@ void* lmdtw_stream(int device) {
     Ctx* c = nullptr;
     if (get_ctx(device, &c) != LMDTW_OK) return nullptr;
     return (void*)c->st;
+}
+
+// Benchmark hook (not part of the reference-facing ABI): `npasses`
+// independent full-grid passes of one strip each (H x N), random features,
+// `reps` launches; *ms = mean kernel time.  Measures the strip engine's
+// per-warp step rate without strip-to-strip dependencies.
+int lmdtw_debug_wave_independent(int device, int32_t precision, int32_t d, int32_t npasses, int32_t N,
+                                 int32_t reps, double* ms) {
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    Engine E(*c, precision, d);
+    const int64_t M = E.H;
+    std::vector<float> hx((size_t)M * d), hy((size_t)N * d);
+    unsigned s = 12345u;
+    for (auto& v : hx) { s = s * 1664525u + 1013904223u; v = (s >> 8) * (1.0f / 16777216.0f); }
+    for (auto& v : hy) { s = s * 1664525u + 1013904223u; v = (s >> 8) * (1.0f / 16777216.0f); }
+    const float* xp = hx.data();
+    const float* yp = hy.data();
+    int64_t Mv = M, Nv = N;
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&xp, &Mv, 1, LMDTW_MEM_HOST, true, xb));
+    TRY(E.stage(&yp, &Nv, 1, LMDTW_MEM_HOST, false, yb));
+    int64_t out_total = 0, bnd_total = 0;
+    std::vector<PassDesc> P;
+    for (int q = 0; q < npasses; q++)
+        P.push_back(E.half_pass_desc(xb[0], yb[0], M, N, M + N - 2, 0, out_total, bnd_total));
+    CU(c->out.ensure((size_t)out_total * E.esz));
+    double tot = 0;
+    for (int r = 0; r < reps + 1; r++) {
+        TRY(E.run_wave(P, bnd_total, false, nullptr, nullptr, 0));
+        CU(cudaEventRecord(c->ev1, c->st));
+        CU(cudaEventSynchronize(c->ev1));
+        if (r == 0) continue;  // warm-up
+    }
+    // time the last `reps` launches as one block
+    CU(cudaEventRecord(c->ev0, c->st));
+    for (int r = 0; r < reps; r++) TRY(E.run_wave(P, bnd_total, false, nullptr, nullptr, 0));
+    CU(cudaEventRecord(c->ev1, c->st));
+    CU(cudaEventSynchronize(c->ev1));
+    float f = 0;
+    CU(cudaEventElapsedTime(&f, c->ev0, c->ev1));
+    tot = f;
+    *ms = tot / reps;
+    return LMDTW_OK;
 }
 
 int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d, int64_t kstop,

@@ -7,8 +7,9 @@ namespace lmdtw {
 
 // Threads per strip-lane: a warp owns a strip of 32*R grid rows.
 constexpr int kWarp = 32;
-// Steps of boundary prefetch (lane 31 feeds lane 0 of the next strip).
-constexpr int kFeedAhead = 8;
+// Zero rows padded before and after the device X / Y arrays: lets the strip
+// engine walk row pointers past the sub-block edges without clamping.
+constexpr int kPadRows = 128;
 
 // One DP domain handled by the strip engine.  For a half pass it is the
 // triangle {i + j <= kstop} of an M x N grid (optionally on the reversed
@@ -21,7 +22,7 @@ struct PassDesc {
     int32_t rows;           // rows taking part: min(M, kstop+1)
     int32_t nstrips;        // ceil(rows / (32 R))
     int64_t out_off[6];     // half pass: D(k-2),D(k-1),D(k),C(k-2),C(k-1),C(k)
-    int64_t bnd_off;        // 2 * N boundary slots (double-buffered strip handoff)
+    int64_t bnd_off;        // 2 slots x N tagged 64-bit words (x2 for fp64): strip handoff
     int64_t bp_off;         // leaf: backpointer words (uint64, 32 cells each)
     int64_t tab_off;        // leaf: optional full D table (-1 = none)
     int32_t w64;            // leaf: words per backpointer row = ceil(N/32)
@@ -70,7 +71,7 @@ struct WaveLaunch {
     int nitems;
     int* counter;           // work queue head (zeroed by caller)
     void* out;              // half-pass diagonal outputs
-    void* bnd;              // strip boundary slots (memset 0xFF by caller)
+    void* bnd;              // strip handoff words (memset 0xFF = tag -1 by caller)
     unsigned long long* bp; // leaf backpointers
     void* tab;              // leaf full tables (may be null)
     void* leaf_cost;        // leaf D[M-1,N-1], one per leaf_id (may be null)

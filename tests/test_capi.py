@@ -89,3 +89,17 @@ def test_compute_without_device_fails_loudly():
         L.dtw_full(X, X)
     with pytest.raises(RuntimeError):
         L.diag_dtw(X, X, kstop=4)
+
+
+def test_no_contracted_packed_fma_in_sass():
+    """Bit parity needs unfused mul/add.  ptxas contracts mul.rn.f32x2 +
+    add.rn.f32x2 into FFMA2, so squares are written as fma(d, d, +0): every
+    FFMA2 in the library must have the zero register as its addend."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run(["cuobjdump", "-sass", _capi.LIB_PATH], capture_output=True, text=True).stdout
+    ffma2 = [l for l in sass.splitlines() if "FFMA2" in l]
+    assert ffma2, "expected packed f32x2 squares in the fp32 kernels"
+    assert all("RZ.F32" in l for l in ffma2), [l for l in ffma2 if "RZ.F32" not in l][:3]
