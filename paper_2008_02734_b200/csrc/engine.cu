@@ -849,7 +849,7 @@ int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64
     TRY(E.stage(&X, &M, 1, mem, true, xb));
     TRY(E.stage(&Y, &N, 1, mem, false, yb));
     int64_t out_total = 0, bnd_total = 0;
-    std::vector<PassDesc> P{E.half_pass_desc(0, 0, M, N, kstop, reverse ? 1 : 0, out_total, bnd_total)};
+    std::vector<PassDesc> P{E.half_pass_desc(xb[0], yb[0], M, N, kstop, reverse ? 1 : 0, out_total, bnd_total)};
     CU(c->out.ensure((size_t)out_total * E.esz));
     const int64_t cl = cells_upto(kstop, M, N);
     TRY(E.run_wave(P, bnd_total, false, nullptr, nullptr, cl));
