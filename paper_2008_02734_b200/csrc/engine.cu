@@ -377,7 +377,7 @@ struct Engine {
             out_total += dlen(kstop - 2 + s, M, N);
         }
         p.bnd_off = bnd_total;
-        bnd_total += 2 * N * bwords();
+        bnd_total += 2 * ((N + 1) & ~1LL) * bwords();  // two slots, 16-byte aligned
         p.bp_off = 0;
         p.tab_off = -1;
         p.w64 = 0;
@@ -465,7 +465,7 @@ struct Engine {
             p.rows = (int32_t)nd.M;
             p.nstrips = (p.rows + H - 1) / H;
             p.bnd_off = bnd_total;
-            bnd_total += 2 * nd.N * bwords();
+            bnd_total += 2 * ((nd.N + 1) & ~1LL) * bwords();  // two slots, 16-byte aligned
             p.w64 = (int32_t)((nd.N + 31) / 32);
             p.bp_off = bp_total;
             bp_total += nd.M * p.w64;
