@@ -117,7 +117,7 @@ struct Ctx {
     std::mutex mu;
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    DBuf xraw, yraw, xp, yp, passes, items, counter, out, bnd, pdesc, pout, ldesc, bp, path, pcost, plen,
+    DBuf xraw, yraw, xp, yp, passes, items, counter, out, bnd, pdesc, pout, pscratch, ldesc, bp, path, pcost, plen,
         lcost, tab;
     HBuf h_passes, h_items, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
     long long call_launches = 0;
@@ -425,8 +425,11 @@ struct Engine {
         CU(c.h_pout.ensure(V.size() * sizeof(PivotOut)));
         memcpy(c.h_pdesc.p, V.data(), V.size() * sizeof(PivotDesc));
         CU(cudaMemcpyAsync(c.pdesc.p, c.h_pdesc.p, V.size() * sizeof(PivotDesc), cudaMemcpyHostToDevice, c.st));
+        const size_t scb = pivot_scratch_bytes((int)V.size());
+        CU(c.pscratch.ensure(scb));
+        CU(cudaMemsetAsync(c.pscratch.p, 0, scb, c.st));  // zeroes the per-node done counters
         TRY(launched(launch_pivots(prec, c.passes.as<PassDesc>(), c.pdesc.as<PivotDesc>(), (int)V.size(), c.out.p,
-                                   c.pout.as<PivotOut>(), c.st),
+                                   c.pout.as<PivotOut>(), c.pscratch.p, c.st),
                      "pivot_kernel"));
         CU(cudaMemcpyAsync(c.h_pout.p, c.pout.p, V.size() * sizeof(PivotOut), cudaMemcpyDeviceToHost, c.st));
         c.d2h += V.size() * sizeof(PivotOut);

@@ -84,7 +84,9 @@ int rows_per_lane(int precision, int dp);
 int supported_dp(int precision, int d);  // padded dim for d, or -1
 cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
 cudaError_t launch_pivots(int precision, const PassDesc* passes, const PivotDesc* piv, int npiv,
-                          const void* out, PivotOut* res, cudaStream_t stream);
+                          const void* out, PivotOut* res, void* scratch, cudaStream_t stream);
+// scratch for launch_pivots; its per-node counters must start at zero
+size_t pivot_scratch_bytes(int npiv);
 cudaError_t launch_backtrace(int precision, int dp, const void* X, const void* Y, const LeafDesc* leaves,
                              int nleaves, const unsigned long long* bp, int* path, void* pcost,
                              int* plen, cudaStream_t stream);
