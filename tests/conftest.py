@@ -13,7 +13,13 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running parity sweep")
     # Build the product library and the oracle once if this checkout lacks them
     # (nvcc cross-compiles without a GPU; gcc builds the oracle).
-    from paper_2008_02734_b200 import build as _b
+    # (build.py is loaded by path: the package itself refuses to import
+    # without its .so)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_lmdtw_build", os.path.join(ROOT, "paper_2008_02734_b200", "build.py"))
+    _b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_b)
     if not os.path.exists(_b.LIB):
         _b.build()
     from oracle import oracle as _o
