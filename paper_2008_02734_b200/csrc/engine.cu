@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -118,7 +119,7 @@ struct Ctx {
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     DBuf xraw, yraw, xp, yp, passes, items, counter, out, bnd, pdesc, pout, pscratch, ldesc, bp, path, pcost, plen,
-        lcost, tab;
+        lcost, tab, trace, lb, flags;
     HBuf h_passes, h_items, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
     long long call_launches = 0;
     long long h2d = 0, d2h = 0;
@@ -144,6 +145,10 @@ int get_ctx(int device, Ctx** out) {
         CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
         CU(cudaEventCreate(&c->ev0));
         CU(cudaEventCreate(&c->ev1));
+        if (const char* w = getenv("LMDTW_WATCHDOG_S")) {
+            const double sec = atof(w);
+            if (sec > 0) CU(set_watchdog_ns((unsigned long long)(sec * 1e9)));
+        }
         g_ctx[device] = std::move(c);
     }
     *out = g_ctx[device].get();
@@ -219,13 +224,12 @@ struct Node {
 
 struct Engine {
     Ctx& c;
-    int prec, d, dp, R, H;
+    int prec, d, dp, H;
     size_t esz;
     int tie[3] = {2, 0, 1};
     Engine(Ctx& ctx, int precision, int dim) : c(ctx), prec(precision), d(dim) {
         dp = supported_dp(prec, d);
-        R = rows_per_lane(prec, dp);
-        H = 32 * R;
+        H = strip_height(prec, dp);
         esz = prec == 32 ? 4 : 8;
     }
 
@@ -274,35 +278,59 @@ struct Engine {
         return LMDTW_OK;
     }
 
-    // Work queue: (pass, strip) ordered by strip length, longest first; ties
-    // by (pass, strip).  Lengths never increase along a pass, so each strip's
-    // predecessor precedes it (the persistent kernel's deadlock freedom).
+    // Work queue of tiles (pass, strip a, column block b), ordered by the
+    // tile's earliest start b*W + a*kLagKey: a strip trails the strip above
+    // it by a short lag and its own previous tile by a tile width, so both
+    // predecessors of a tile come earlier in the queue -- the persistent
+    // kernel's deadlock freedom -- and pipelines rotate over the strips
+    // instead of holding a long strip while shorter ones wait behind it.
+    static constexpr int64_t kLagKey = 128;
+    static int64_t tiles_of(const PassDesc& p, int a, int H) {
+        const int64_t jend = std::min<int64_t>(p.N - 1, (int64_t)p.kstop - (int64_t)a * H);
+        return jend / kTileW + 1;
+    }
     void make_items(const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
-        int64_t total = 0, maxlen = 0;
-        for (const auto& p : P) {
-            total += p.nstrips;
-            maxlen = std::max<int64_t>(maxlen, p.N + 32);
-        }
-        auto len_of = [&](const PassDesc& p, int a) -> int64_t {
-            int64_t je = std::min<int64_t>(p.N - 1, (int64_t)p.kstop - (int64_t)a * H);
-            return je + 32;
-        };
-        std::vector<int64_t> cnt(maxlen + 2, 0);
+        // key = b*W + a*kLagKey = kLagKey * (b*(W/kLagKey) + a): a counting sort on
+        // m = b*(W/kLagKey) + a, stable in (pass, strip, block) generation order
+        static_assert(kTileW % kLagKey == 0, "tile width must be a multiple of the key lag");
+        constexpr int64_t kPer = kTileW / kLagKey;
+        int64_t mmax = 0, total = 0;
+        for (const auto& p : P)
+            for (int a = 0; a < p.nstrips; a++) {
+                const int64_t nb = tiles_of(p, a, H);
+                mmax = std::max<int64_t>(mmax, (nb - 1) * kPer + a);
+                total += nb;
+            }
+        std::vector<int64_t> cnt(mmax + 2, 0);
+        for (const auto& p : P)
+            for (int a = 0; a < p.nstrips; a++) {
+                const int64_t nb = tiles_of(p, a, H);
+                for (int64_t b = 0; b < nb; b++) cnt[b * kPer + a + 1]++;
+            }
+        for (int64_t m = 1; m <= mmax + 1; m++) cnt[m] += cnt[m - 1];
+        items.resize(total);
         for (size_t q = 0; q < P.size(); q++)
-            for (int a = 0; a < P[q].nstrips; a++) cnt[maxlen - len_of(P[q], a)]++;
-        int64_t acc = 0;
-        for (auto& v : cnt) {
-            int64_t t = v;
-            v = acc;
-            acc += t;
-        }
-        items.assign(total, WorkItem{0, 0});
-        for (size_t q = 0; q < P.size(); q++)
-            for (int a = 0; a < P[q].nstrips; a++) items[cnt[maxlen - len_of(P[q], a)]++] = WorkItem{(int)q, a};
+            for (int a = 0; a < P[q].nstrips; a++) {
+                const int64_t nb = tiles_of(P[q], a, H);
+                for (int64_t b = 0; b < nb; b++) items[cnt[b * kPer + a]++] = WorkItem{(int)q, a, (int)b, 0};
+            }
     }
 
-    int run_wave(const std::vector<PassDesc>& P, int64_t bnd_total, bool leaf, void* tab, void* lcost,
+    int run_wave(const std::vector<PassDesc>& P0, int64_t bnd_total, bool leaf, void* tab, void* lcost,
                  int64_t cells) {
+        // tile bookkeeping: per strip H+1 boundary values and a completion count
+        std::vector<PassDesc> P(P0);
+        int64_t lb_total = 0, flag_total = 0;
+        for (auto& p : P) {
+            p.tile_w = kTileW;
+            p.lb_off = lb_total;
+            p.flag_off = flag_total;
+            lb_total += (int64_t)p.nstrips * (H + 1);
+            flag_total += p.nstrips;
+        }
+        CU(c.lb.ensure((size_t)std::max<int64_t>(lb_total, 1) * esz));
+        CU(c.flags.ensure((size_t)std::max<int64_t>(flag_total, 1) * sizeof(int)));
+        CU(cudaMemsetAsync(c.flags.p, 0, (size_t)std::max<int64_t>(flag_total, 1) * sizeof(int), c.st));
         std::vector<WorkItem> items;
         make_items(P, items);
         CU(c.h_passes.ensure(P.size() * sizeof(PassDesc)));
@@ -329,6 +357,8 @@ struct Engine {
         w.out = c.out.p;
         w.bnd = c.bnd.p;
         w.bp = c.bp.as<unsigned long long>();
+        w.lb = c.lb.p;
+        w.flags = c.flags.as<int>();
         w.tab = tab;
         w.leaf_cost = lcost;
         w.tie0 = tie[0];
@@ -336,9 +366,29 @@ struct Engine {
         w.tie2 = tie[2];
         w.leaf = leaf ? 1 : 0;
         w.grid_warps = 0;
+        // LMDTW_TRACE_FILE: append per-strip DP start/end timestamps (debug)
+        const char* trace_file = getenv("LMDTW_TRACE_FILE");
+        if (trace_file) {
+            CU(c.trace.ensure(items.size() * 24));
+            CU(cudaMemsetAsync(c.trace.p, 0, items.size() * 24, c.st));
+            w.trace = c.trace.as<unsigned long long>();
+        }
         const bool prof = g_profile.load() != 0;
         if (prof) CU(cudaEventRecord(c.ev0, c.st));
         TRY(launched(launch_wave(w, c.st), leaf ? "leaf wave_kernel" : "wave_kernel"));
+        if (trace_file) {
+            std::vector<unsigned long long> tr(items.size() * 3);
+            CU(cudaMemcpyAsync(tr.data(), c.trace.p, tr.size() * 8, cudaMemcpyDeviceToHost, c.st));
+            CU(cudaStreamSynchronize(c.st));
+            if (FILE* f = fopen(trace_file, "ab")) {
+                const long long hdr[3] = {(long long)P.size(), (long long)items.size(), (long long)leaf};
+                fwrite(hdr, sizeof hdr, 1, f);
+                fwrite(P.data(), sizeof(PassDesc), P.size(), f);
+                fwrite(items.data(), sizeof(WorkItem), items.size(), f);
+                fwrite(tr.data(), 8, tr.size(), f);
+                fclose(f);
+            }
+        }
         if (prof) {
             CU(cudaEventRecord(c.ev1, c.st));
             CU(cudaEventSynchronize(c.ev1));

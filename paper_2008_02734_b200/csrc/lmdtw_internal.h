@@ -5,11 +5,9 @@
 
 namespace lmdtw {
 
-// Threads per strip-lane: a warp owns a strip of 32*R grid rows.
-constexpr int kWarp = 32;
 // Zero rows padded before and after the device X / Y arrays: lets the strip
 // engine walk row pointers past the sub-block edges without clamping.
-constexpr int kPadRows = 128;
+constexpr int kPadRows = 256;
 
 // One DP domain handled by the strip engine.  For a half pass it is the
 // triangle {i + j <= kstop} of an M x N grid (optionally on the reversed
@@ -27,11 +25,23 @@ struct PassDesc {
     int64_t tab_off;        // leaf: optional full D table (-1 = none)
     int32_t w64;            // leaf: words per backpointer row = ceil(N/32)
     int32_t leaf_id;        // leaf: index into per-leaf outputs
+    int64_t lb_off;         // tile left boundaries: nstrips x (H + 1) values (set by the launcher)
+    int64_t flag_off;       // tiles completed per strip: nstrips ints (set by the launcher)
+    int32_t tile_w;         // columns per tile (set by the launcher)
+    int32_t pad;
 };
 
+// Columns per work item: a strip is cut into tiles of kTileW columns so the
+// persistent pipelines rotate over strips instead of holding one strip for
+// its whole length (a multiple of 32 and of the ring chunk).
+constexpr int kTileW = 2048;
+
+// One tile: strip `strip` of pass `pass`, columns [blk * tile_w, ...).
 struct WorkItem {
     int32_t pass;
     int32_t strip;
+    int32_t blk;
+    int32_t pad;
 };
 
 // Pivot search input: the two passes of one internal node.
@@ -77,10 +87,13 @@ struct WaveLaunch {
     void* leaf_cost;        // leaf D[M-1,N-1], one per leaf_id (may be null)
     int tie0, tie1, tie2;
     int leaf;               // 0 half pass, 1 leaf fill
+    void* lb;               // tile left boundaries (dtype T)
+    int* flags;             // tiles completed per strip (zeroed by caller)
     int grid_warps;         // persistent warps to launch (0 = auto)
+    unsigned long long* trace;  // optional per-item timestamps (debug)
 };
 
-int rows_per_lane(int precision, int dp);
+int strip_height(int precision, int dp);  // grid rows per strip
 int supported_dp(int precision, int d);  // padded dim for d, or -1
 cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
 cudaError_t launch_pivots(int precision, const PassDesc* passes, const PivotDesc* piv, int npiv,
@@ -93,5 +106,6 @@ cudaError_t launch_backtrace(int precision, int dp, const void* X, const void* Y
 cudaError_t launch_pad_cast(int precision, const float* src, int64_t rows, int d, int dp, void* dst,
                             cudaStream_t stream);
 int max_resident_warps(int precision, int dp, int leaf, int device);
+cudaError_t set_watchdog_ns(unsigned long long ns);  // per device (current device)
 
 }  // namespace lmdtw
