@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: ptxas otherwise fuses mul.rn.f32x2 + add.rn.f32x2 into FFMA2,
 # breaking bit parity; -ffp-contract=off: same rule for host-side path_cost.
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
-         "-Xptxas", "-warn-spills", "-I", CSRC, "-I", INCLUDE]
+         "-Xptxas", "-warn-spills", "-I", CSRC, "-I", INCLUDE] + os.environ.get("LMDTW_NVCC_EXTRA", "").split()
 
 
 def _stale(target, deps):

@@ -358,6 +358,7 @@ struct Engine {
         w.bnd = c.bnd.p;
         w.bp = c.bp.as<unsigned long long>();
         w.lb = c.lb.p;
+        if (const char* d = getenv("LMDTW_PROBE")) w.dbg = atoi(d);  // LMDTW_PROBES builds only
         w.flags = c.flags.as<int>();
         w.tab = tab;
         w.leaf_cost = lcost;

@@ -89,6 +89,7 @@ struct WaveLaunch {
     int leaf;               // 0 half pass, 1 leaf fill
     void* lb;               // tile left boundaries (dtype T)
     int* flags;             // tiles completed per strip (zeroed by caller)
+    int dbg;                // probe mode (LMDTW_PROBES builds; 0 = normal)
     int grid_warps;         // persistent warps to launch (0 = auto)
     unsigned long long* trace;  // optional per-item timestamps (debug)
 };
