@@ -338,11 +338,17 @@ def run_ours(args, rank, world):
     f_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     roof = fp32_cell_roofline(d, n_sm, f_mhz)
     wave_rate = prof["wave_cells"] / (prof["wave_ms"] / 1e3) if prof["wave_ms"] > 0 else 0.0
-    traffic = None
+    # dram bytes per launch of the dominant kernel (level-0 wave_kernel) from one
+    # ncu --set full capture, committed under profiles/ (null if not captured)
+    traffic, traffic_basis = None, None
     tp = os.path.join(ROOT, "profiles", "wave_kernel_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config)
+            t = json.load(open(tp)).get(args.config)
+            if t:
+                traffic = t["per_launch_bytes"]
+                traffic_basis = (f"{t['launch']}: dram read+write per launch for {t['cells']} cells; algorithmic: "
+                                 f"X+Y features once + 6 output diagonals ~= {t.get('algorithmic_bytes', 'n/a')} B")
         except Exception:
             traffic = None
 
@@ -359,7 +365,7 @@ def run_ours(args, rank, world):
                 "api": "paper_2008_02734_b200.linmdtw (pinned host FeatureSeries)"},
         "roofline": {"bound": "fp32", "kernel": "wave_kernel (half passes)", "achieved": round(wave_rate / 1e9, 2),
                      "peak": round(roof / 1e9, 2), "unit": "Gcell/s", "frac": round(wave_rate / roof, 4),
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_basis": traffic_basis,
                      "peak_basis": f"N_SM={n_sm} x 128 lanes x {f_mhz} MHz ({kind} sm_max_mhz) / (2d+5), d={d}",
                      "kernel_ms_share": round(prof["wave_ms"] / sum(ms), 4) if sum(ms) > 0 else None},
         "clocks": clocks,
