@@ -18,6 +18,13 @@
  *   lmdtw_align_batch == many independent linmdtw calls fused level by level
  *   lmdtw_path_cost   == core.path_cost         (core.py:182-197)
  *
+ * Building blocks of the multi-GPU recursion (paper_2008_02734_b200/
+ * distributed.py): one recursion level's find_pivot calls on sub-blocks
+ * (lmdtw_pivot_nodes == divide.find_pivot on X.view/Y.view, divide.py:158-167),
+ * the leaf dtw_full calls (lmdtw_leaf_nodes == divide._solve's leaf branch,
+ * divide.py:153-157), and the split-point combine of two half passes computed
+ * on different GPUs (lmdtw_pivot_combine == divide.py:122-145).
+ *
  * Memory: every entry takes `mem`: LMDTW_MEM_HOST means X/Y/outputs are host
  * pointers (the library stages them through pinned memory, copies included in
  * the call); LMDTW_MEM_DEVICE means X/Y are device pointers on `device`
@@ -135,6 +142,28 @@ int lmdtw_align(int device, const float *X, int64_t M, const float *Y, int64_t N
 int lmdtw_align_batch(int device, int32_t npairs, const float *const *X, const int64_t *M,
                       const float *const *Y, const int64_t *N, int32_t d,
                       const lmdtw_config_t *cfg, int32_t mem, lmdtw_result_t **results);
+
+/* find_pivot on n sub-blocks sub[4q..4q+3] = (i_off, j_off, Mq, Nq) of X x Y
+ * in one batched launch: out[5q..5q+4] = (i, j, diagonal_k, cells, peak) in
+ * sub-block coordinates, totals[q] = total_at_pivot. */
+int lmdtw_pivot_nodes(int device, const float *X, int64_t M, const float *Y, int64_t N, int32_t d,
+                      int32_t n, const int64_t *sub, int32_t precision, int32_t pivot_highest,
+                      int32_t mem, int64_t *out, double *totals);
+
+/* dtw_full on n sub-blocks in one batched launch: the local paths (forward
+ * order, sub-block coordinates) are concatenated into path_out (room for
+ * sum(Mq + Nq - 1) (i,j) int64 pairs), path_len[q] = Kq. */
+int lmdtw_leaf_nodes(int device, const float *X, int64_t M, const float *Y, int64_t N, int32_t d,
+                     int32_t n, const int64_t *sub, const int32_t tie[3], int32_t precision,
+                     int32_t mem, int64_t *path_out, int64_t *path_len);
+
+/* Split point from a forward and a reverse half pass computed elsewhere (host
+ * buffers from lmdtw_half_pass: fwd to kf = ceil((M+N-1)/2), reverse to kb):
+ * (Df + Db[idx_b]) - Cf with the lexicographic (value, k, idx) argmin
+ * ("lowest") or (value, -k, -idx) ("highest").  ijk = (i, j, diagonal_k). */
+int lmdtw_pivot_combine(int32_t precision, int64_t M, int64_t N, int32_t pivot_highest,
+                        const void *const fwd_d[3], const void *const fwd_c[3],
+                        const void *const bwd_d[3], int64_t *ijk, double *total);
 
 int lmdtw_result_info(const lmdtw_result_t *r, lmdtw_align_info_t *info);
 /* Copies K (i,j) int64 pairs. */

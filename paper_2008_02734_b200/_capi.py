@@ -44,7 +44,8 @@ EXPORTS = (
     "lmdtw_half_pass", "lmdtw_find_pivot", "lmdtw_dtw_full", "lmdtw_align",
     "lmdtw_align_batch", "lmdtw_result_info", "lmdtw_result_path", "lmdtw_result_pivots",
     "lmdtw_result_free", "lmdtw_path_cost", "lmdtw_diag_length", "lmdtw_cells_upto",
-    "lmdtw_peak_retained_values", "lmdtw_launch_count",
+    "lmdtw_peak_retained_values", "lmdtw_launch_count", "lmdtw_pivot_nodes", "lmdtw_leaf_nodes",
+    "lmdtw_pivot_combine",
 )
 
 _lib = None
@@ -85,6 +86,12 @@ def load():
     L.lmdtw_result_pivots.restype = C.c_int
     L.lmdtw_result_free.argtypes = [P]
     L.lmdtw_result_free.restype = None
+    L.lmdtw_pivot_nodes.argtypes = [C.c_int, P, I64, P, I64, I32, I32, P, I32, I32, I32, P, P]
+    L.lmdtw_pivot_nodes.restype = C.c_int
+    L.lmdtw_leaf_nodes.argtypes = [C.c_int, P, I64, P, I64, I32, I32, P, P, I32, I32, P, P]
+    L.lmdtw_leaf_nodes.restype = C.c_int
+    L.lmdtw_pivot_combine.argtypes = [I32, I64, I64, I32, P, P, P, P, P]
+    L.lmdtw_pivot_combine.restype = C.c_int
     L.lmdtw_path_cost.argtypes = [P, I64, P, I64, I32, P, I64, I32, P]
     L.lmdtw_path_cost.restype = C.c_int
     for f in ("lmdtw_diag_length", "lmdtw_cells_upto", "lmdtw_peak_retained_values"):

@@ -798,6 +798,50 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
 
 }  // namespace
 
+// Host split-point combine of divide.find_pivot (divide.py:122-145) for two
+// half passes computed on different devices.
+namespace {
+template <typename T>
+void combine_pivot(int64_t M, int64_t N, int highest, const void* const fd[3], const void* const fc[3],
+                   const void* const bd[3], int64_t* ijk, double* total) {
+    const int64_t K = M + N - 1;
+    const int64_t kf = (K + 1) / 2;
+    T best = T(0);
+    int64_t bk = -1, bidx = -1;
+    bool have = false;
+    for (int m = 0; m < 3; m++) {
+        const int64_t k = kf - 2 + m;
+        const int64_t L = dlen(k, M, N);
+        const T* df = static_cast<const T*>(fd[m]);
+        const T* cf = static_cast<const T*>(fc[m]);
+        const T* db = static_cast<const T*>(bd[2 - m]);
+        for (int64_t idx = 0; idx < L; idx++) {
+            const int64_t i = std::min(k, M - 1) - idx;
+            const int64_t ib = std::min(M + N - 2 - k, M - 1) - (M - 1 - i);
+            T t = df[idx] + db[ib];  // two roundings in the reference's order
+            t = t - cf[idx];
+            // lexicographic (t, k, idx) minimum, or (t, -k, -idx) for "highest"
+            bool take;
+            if (!have) take = true;
+            else if (t < best) take = true;
+            else if (t == best) take = highest ? (k > bk || (k == bk && idx > bidx)) : false;
+            else take = false;
+            if (take) {
+                best = t;
+                bk = k;
+                bidx = idx;
+                have = true;
+            }
+        }
+    }
+    const int64_t i = std::min(bk, M - 1) - bidx;
+    ijk[0] = i;
+    ijk[1] = bk - i;
+    ijk[2] = bk;
+    *total = (double)best;
+}
+}  // namespace
+
 // ====================================================================== C ABI
 extern "C" {
 
@@ -1006,6 +1050,115 @@ int lmdtw_align_batch(int device, int32_t npairs, const float* const* X, const i
     std::vector<lmdtw_result*> res;
     TRY(align_core(device, npairs, X, M, Y, N, d, *cfg, mem, nullptr, nullptr, res));
     for (int p = 0; p < npairs; p++) results[p] = res[p];
+    return LMDTW_OK;
+}
+
+int lmdtw_pivot_nodes(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d, int32_t n,
+                      const int64_t* sub, int32_t precision, int32_t pivot_highest, int32_t mem, int64_t* out,
+                      double* totals) {
+    TRY(validate_common(M, N, d, precision));
+    if (n < 0 || (n > 0 && (!sub || !out || !totals))) return set_err(LMDTW_EINVAL, "bad node list");
+    for (int q = 0; q < n; q++) {
+        const int64_t* s = sub + 4 * q;
+        if (s[0] < 0 || s[1] < 0 || s[2] < 1 || s[3] < 1 || s[0] + s[2] > M || s[1] + s[3] > N)
+            return set_err(LMDTW_EINVAL, "sub-block outside the series");
+        if (s[2] + s[3] - 2 < 2) return set_err(LMDTW_EINVAL, "sub-block too small for a pivot search");
+    }
+    if (n == 0) return LMDTW_OK;
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    c->call_launches = 0;
+    Engine E(*c, precision, d);
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&X, &M, 1, mem, true, xb));
+    TRY(E.stage(&Y, &N, 1, mem, false, yb));
+    std::vector<Node> nodes(n);
+    std::vector<int> ids(n);
+    for (int q = 0; q < n; q++) {
+        nodes[q].i_off = sub[4 * q];
+        nodes[q].j_off = sub[4 * q + 1];
+        nodes[q].M = sub[4 * q + 2];
+        nodes[q].N = sub[4 * q + 3];
+        nodes[q].pair = 0;
+        ids[q] = q;
+    }
+    std::vector<int64_t> cl, pk;
+    TRY(E.pivot_level(nodes, ids, xb, yb, &cl, &pk, pivot_highest ? 1 : 0));
+    for (int q = 0; q < n; q++) {
+        out[5 * q] = nodes[q].pi;
+        out[5 * q + 1] = nodes[q].pj;
+        out[5 * q + 2] = nodes[q].k;
+        out[5 * q + 3] = cl[q];
+        out[5 * q + 4] = pk[q];
+        totals[q] = nodes[q].total;
+    }
+    return LMDTW_OK;
+}
+
+int lmdtw_leaf_nodes(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d, int32_t n,
+                     const int64_t* sub, const int32_t tie[3], int32_t precision, int32_t mem, int64_t* path_out,
+                     int64_t* path_len) {
+    TRY(validate_common(M, N, d, precision));
+    TRY(validate_tie(tie));
+    if (n < 0 || (n > 0 && (!sub || !path_out || !path_len))) return set_err(LMDTW_EINVAL, "bad node list");
+    for (int q = 0; q < n; q++) {
+        const int64_t* s = sub + 4 * q;
+        if (s[0] < 0 || s[1] < 0 || s[2] < 1 || s[3] < 1 || s[0] + s[2] > M || s[1] + s[3] > N)
+            return set_err(LMDTW_EINVAL, "sub-block outside the series");
+    }
+    if (n == 0) return LMDTW_OK;
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    c->call_launches = 0;
+    Engine E(*c, precision, d);
+    E.tie[0] = tie[0];
+    E.tie[1] = tie[1];
+    E.tie[2] = tie[2];
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&X, &M, 1, mem, true, xb));
+    TRY(E.stage(&Y, &N, 1, mem, false, yb));
+    std::vector<Node> nodes(n);
+    std::vector<int> ids(n);
+    for (int q = 0; q < n; q++) {
+        nodes[q].i_off = sub[4 * q];
+        nodes[q].j_off = sub[4 * q + 1];
+        nodes[q].M = sub[4 * q + 2];
+        nodes[q].N = sub[4 * q + 3];
+        nodes[q].pair = 0;
+        ids[q] = q;
+    }
+    std::vector<int64_t> poff;
+    std::vector<int> plen;
+    TRY(E.leaves(nodes, ids, xb, yb, nullptr, poff, plen));
+    const int* hp = c->h_path.as<int>();
+    int64_t w = 0;
+    for (int q = 0; q < n; q++) {
+        const int len = plen[q];
+        const int* lp = hp + 2 * poff[q];  // reversed: lp[0] is the corner
+        for (int t = 0; t < len; t++) {
+            path_out[2 * (w + t)] = lp[2 * (len - 1 - t)];
+            path_out[2 * (w + t) + 1] = lp[2 * (len - 1 - t) + 1];
+        }
+        path_len[q] = len;
+        w += len;
+    }
+    return LMDTW_OK;
+}
+
+
+int lmdtw_pivot_combine(int32_t precision, int64_t M, int64_t N, int32_t pivot_highest, const void* const fwd_d[3],
+                        const void* const fwd_c[3], const void* const bwd_d[3], int64_t* ijk, double* total) {
+    if (precision != 32 && precision != 64) return set_err(LMDTW_EINVAL, "precision must be 32 or 64");
+    if (M < 1 || N < 1 || M + N - 2 < 2) return set_err(LMDTW_EINVAL, "too small for a pivot search");
+    if (!fwd_d || !fwd_c || !bwd_d || !ijk || !total) return set_err(LMDTW_EINVAL, "null buffer");
+    if (precision == 32)
+        combine_pivot<float>(M, N, pivot_highest, fwd_d, fwd_c, bwd_d, ijk, total);
+    else
+        combine_pivot<double>(M, N, pivot_highest, fwd_d, fwd_c, bwd_d, ijk, total);
     return LMDTW_OK;
 }
 

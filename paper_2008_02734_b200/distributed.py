@@ -1,0 +1,277 @@
+"""Exact linear-memory DTW across the GPUs of one box.
+
+One process per GPU (torch.distributed; NCCL on the GPU box, gloo in the CPU
+tests).  The recursion of divide._solve (divide.py:148-178) runs level by
+level on every rank with identical bookkeeping; only the compute is split:
+
+* A recursion level with at least as many internal nodes as ranks hands each
+  rank a set of whole nodes, longest-processing-time first by cell count; a
+  rank solves its nodes' find_pivot calls in one batched launch
+  (lmdtw_pivot_nodes) and the pivots are exchanged (all_gather).
+* A level with fewer nodes than ranks (the top of the tree: one node at
+  level 0) is split one step further, into the nodes' forward and reverse
+  half passes (diagonal.diag_dtw, diagonal.py:172-223), again assigned
+  longest-first.  The owners exchange the three returned diagonals and every
+  rank applies the split-point combine of divide.find_pivot
+  (divide.py:122-145; lmdtw_pivot_combine) to the same data.
+* Leaves (divide.py:153-157) are sharded the same way; their paths are
+  exchanged and stitched in the reference's pre-order.
+
+The returned AlignmentResult (path, cost = core.path_cost, cells_processed,
+peak_diag_values, peak_table_cells, pivot_trace) is identical to
+divide.linmdtw's -- the partition never changes what is computed, only where.
+The only data-path exchange is pivots, half-pass diagonals and leaf paths
+(O(M + N) per level); features are replicated on every rank.
+
+The compute backend is pluggable: ``DeviceEngine`` drives the C ABI on this
+rank's GPU.  The CPU tests drive the same driver with a test engine to check
+the partition and exchange logic under gloo.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _capi
+from .core import AlignmentResult, InvalidInputError, as_series, check_cost_kind, precision_dtype
+from .divide import LinMdtwConfig, _c_config
+from .textbook import tie_codes
+
+
+def lpt_assign(weights, world):
+    """Longest-processing-time assignment: unit q -> rank, deterministic on
+    every rank (ties: lower unit index first, then the lowest loaded rank)."""
+    load = [0] * world
+    owner = [0] * len(weights)
+    for q in sorted(range(len(weights)), key=lambda q: (-int(weights[q]), q)):
+        r = min(range(world), key=lambda r: (load[r], r))
+        owner[q] = r
+        load[r] += int(weights[q])
+    return owner
+
+
+def _cells_upto(kstop, M, N):
+    return int(_capi.load().lmdtw_cells_upto(int(kstop), int(M), int(N)))
+
+
+def _peak(kstop, M, N):
+    return int(_capi.load().lmdtw_peak_retained_values(int(kstop), int(M), int(N)))
+
+
+def _kstops(M, N):
+    """find_pivot's forward / reverse stopping diagonals (divide.py:112-114)."""
+    K = M + N - 1
+    kf = (K + 1) // 2
+    kb = kf + 1 if K % 2 == 0 else kf
+    return kf, kb
+
+
+class DeviceEngine:
+    """This rank's compute through the C ABI, features resident on its GPU."""
+
+    def __init__(self, X: np.ndarray, Y: np.ndarray, cfg: LinMdtwConfig, device: int):
+        import torch
+        self.device = int(device)
+        self.cfg = cfg
+        self.prec = 32 if precision_dtype(cfg.precision) == np.float32 else 64
+        self.Xh = np.ascontiguousarray(X, dtype=np.float32)
+        self.Yh = np.ascontiguousarray(Y, dtype=np.float32)
+        self.d = self.Xh.shape[1]
+        self.Xd = torch.from_numpy(self.Xh).to(f"cuda:{self.device}")
+        self.Yd = torch.from_numpy(self.Yh).to(f"cuda:{self.device}")
+        self.lib = _capi.load()
+
+    def _xy(self):
+        return (C.c_void_p(self.Xd.data_ptr()), self.Xh.shape[0], C.c_void_p(self.Yd.data_ptr()),
+                self.Yh.shape[0])
+
+    def pivot_nodes(self, subs):
+        """[(i_off, j_off, M, N)] -> [(i, j, k, total)] (sub-block coordinates)."""
+        n = len(subs)
+        if n == 0:
+            return []
+        sub = np.ascontiguousarray(np.asarray(subs, np.int64).reshape(n, 4))
+        out = np.zeros((n, 5), np.int64)
+        tot = np.zeros(n, np.float64)
+        X, M, Y, N = self._xy()
+        _capi.check(self.lib.lmdtw_pivot_nodes(
+            self.device, X, M, Y, N, self.d, n, _capi.ptr(sub), self.prec,
+            1 if self.cfg.pivot_tie_rule == "highest" else 0, _capi.MEM_DEVICE, _capi.ptr(out), _capi.ptr(tot)))
+        return [(int(out[q, 0]), int(out[q, 1]), int(out[q, 2]), float(tot[q])) for q in range(n)]
+
+    def half_pass(self, sub, reverse):
+        """Three D and three C diagonals of one half pass of find_pivot on the
+        sub-block (diagonal.diag_dtw): forward to kf, reverse to kb."""
+        i_off, j_off, M, N = sub
+        kf, kb = _kstops(M, N)
+        kstop = kb if reverse else kf
+        dt = np.float32 if self.prec == 32 else np.float64
+        lens = [int(self.lib.lmdtw_diag_length(kstop - 2 + s, M, N)) for s in range(3)]
+        d = [np.empty(max(L, 1), dt) for L in lens]
+        c = [np.empty(max(L, 1), dt) for L in lens]
+        pd = (C.c_void_p * 3)(*[a.ctypes.data for a in d])
+        pc = (C.c_void_p * 3)(*[a.ctypes.data for a in c])
+        cells = C.c_int64()
+        Xs = self.Xd[i_off:i_off + M]
+        Ys = self.Yd[j_off:j_off + N]
+        _capi.check(self.lib.lmdtw_half_pass(
+            self.device, C.c_void_p(Xs.data_ptr()), M, C.c_void_p(Ys.data_ptr()), N, self.d, kstop,
+            1 if reverse else 0, self.prec, _capi.MEM_DEVICE, pd, pc, C.byref(cells)))
+        return [d[s][:lens[s]] for s in range(3)], [c[s][:lens[s]] for s in range(3)]
+
+    def combine(self, M, N, fwd_d, fwd_c, bwd_d):
+        """Split point from the two halves (divide.py:122-145)."""
+        fd = (C.c_void_p * 3)(*[np.ascontiguousarray(a).ctypes.data for a in fwd_d])
+        fc = (C.c_void_p * 3)(*[np.ascontiguousarray(a).ctypes.data for a in fwd_c])
+        bd = (C.c_void_p * 3)(*[np.ascontiguousarray(a).ctypes.data for a in bwd_d])
+        ijk = np.zeros(3, np.int64)
+        tot = C.c_double()
+        _capi.check(self.lib.lmdtw_pivot_combine(self.prec, M, N, 1 if self.cfg.pivot_tie_rule == "highest" else 0,
+                                                 fd, fc, bd, _capi.ptr(ijk), C.byref(tot)))
+        return int(ijk[0]), int(ijk[1]), int(ijk[2]), float(tot.value)
+
+    def leaves(self, subs):
+        """[(i_off, j_off, M, N)] -> local forward paths (K, 2) int64."""
+        n = len(subs)
+        if n == 0:
+            return []
+        sub = np.ascontiguousarray(np.asarray(subs, np.int64).reshape(n, 4))
+        cap = int(sum(M + N - 1 for _, _, M, N in subs))
+        path = np.zeros((cap, 2), np.int64)
+        plen = np.zeros(n, np.int64)
+        tie = np.ascontiguousarray(tie_codes(self.cfg.tie_rule), dtype=np.int32)
+        X, M, Y, N = self._xy()
+        _capi.check(self.lib.lmdtw_leaf_nodes(self.device, X, M, Y, N, self.d, n, _capi.ptr(sub),
+                                              _capi.ptr(tie), self.prec, _capi.MEM_DEVICE, _capi.ptr(path),
+                                              _capi.ptr(plen)))
+        out, w = [], 0
+        for q in range(n):
+            out.append(path[w:w + int(plen[q])].copy())
+            w += int(plen[q])
+        return out
+
+    def path_cost(self, path):
+        cost = C.c_double()
+        p = np.ascontiguousarray(path, np.int64)
+        _capi.check(self.lib.lmdtw_path_cost(_capi.ptr(self.Xh), self.Xh.shape[0], _capi.ptr(self.Yh),
+                                             self.Yh.shape[0], self.d, _capi.ptr(p), p.shape[0], self.prec,
+                                             C.byref(cost)))
+        return float(cost.value)
+
+
+def _all_gather(obj, group):
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | None = None, group=None,
+                        engine=None, **overrides) -> AlignmentResult:
+    """divide.linmdtw (divide.py:181-213) with the recursion's compute spread
+    over the ranks of ``group`` (default: the world).  Every rank returns the
+    same AlignmentResult."""
+    import torch.distributed as dist
+    check_cost_kind(cost)
+    cfg = config or LinMdtwConfig(**overrides)
+    if config is not None and overrides:
+        raise InvalidInputError("pass either a config object or keyword overrides, not both")
+    Xs, Ys = as_series(X), as_series(Y)
+    if Xs.dim != Ys.dim:
+        raise InvalidInputError(f"feature dimension mismatch: {Xs.dim} vs {Ys.dim}")
+    _c_config(cfg)  # validates the tie rule
+    M, N = len(Xs), len(Ys)
+    dtype = precision_dtype(cfg.precision)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if engine is None:
+        engine = DeviceEngine(Xs.frames, Ys.frames, cfg, _capi.get_device())
+
+    # node: [i_off, j_off, M, N, left, right, pi, pj, k, total, leaf]
+    nodes = [[0, 0, M, N, -1, -1, -1, -1, -1, 0.0, -1]]
+    level, leaves = [0], []
+    cells, peak_diag, peak_table, nlevels = 0, 0, 0, 0
+    while level:
+        internal = []
+        for q in level:
+            _, _, m, n = nodes[q][:4]
+            if m < cfg.min_dim or n < cfg.min_dim or m + n <= 5:
+                nodes[q][10] = len(leaves)
+                leaves.append(q)
+            else:
+                internal.append(q)
+        if not internal:
+            break
+        nlevels += 1
+        subs = [tuple(nodes[q][:4]) for q in internal]
+        if len(internal) >= world:
+            # whole nodes, longest first
+            w = [_cells_upto(_kstops(m, n)[0], m, n) + _cells_upto(_kstops(m, n)[1], m, n) for _, _, m, n in subs]
+            owner = lpt_assign(w, world)
+            mine = [q for q in range(len(subs)) if owner[q] == rank]
+            res = engine.pivot_nodes([subs[q] for q in mine])
+            got = {}
+            for part in _all_gather(list(zip(mine, res)), group):
+                got.update(dict(part))
+            piv = [got[q] for q in range(len(subs))]
+        else:
+            # forward and reverse half passes as separate units
+            units = [(q, rev) for q in range(len(subs)) for rev in (0, 1)]
+            w = [_cells_upto(_kstops(*subs[q][2:])[rev], *subs[q][2:]) for q, rev in units]
+            owner = lpt_assign(w, world)
+            mine = [u for u in range(len(units)) if owner[u] == rank]
+            res = {u: engine.half_pass(subs[units[u][0]], units[u][1]) for u in mine}
+            got = {}
+            for part in _all_gather(res, group):
+                got.update(part)
+            piv = []
+            for q in range(len(subs)):
+                fd, fc = got[2 * q]
+                bd, _ = got[2 * q + 1]
+                piv.append(engine.combine(subs[q][2], subs[q][3], fd, fc, bd))
+        nxt = []
+        for q, (pi, pj, k, tot) in zip(internal, piv):
+            i_off, j_off, m, n = nodes[q][:4]
+            kf, kb = _kstops(m, n)
+            cells += _cells_upto(kf, m, n) + _cells_upto(kb, m, n)
+            peak_diag = max(peak_diag, _peak(kf, m, n), _peak(kb, m, n))
+            nodes[q][6:10] = [pi, pj, k, tot]
+            nodes.append([i_off, j_off, pi + 1, pj + 1, -1, -1, -1, -1, -1, 0.0, -1])
+            nodes[q][4] = len(nodes) - 1
+            nodes.append([i_off + pi, j_off + pj, m - pi, n - pj, -1, -1, -1, -1, -1, 0.0, -1])
+            nodes[q][5] = len(nodes) - 1
+            nxt += [nodes[q][4], nodes[q][5]]
+        level = nxt
+
+    # leaves, longest first
+    lsubs = [tuple(nodes[q][:4]) for q in leaves]
+    owner = lpt_assign([m * n for _, _, m, n in lsubs], world)
+    mine = [q for q in range(len(lsubs)) if owner[q] == rank]
+    got = {}
+    for part in _all_gather(dict(zip(mine, engine.leaves([lsubs[q] for q in mine]))), group):
+        got.update(part)
+
+    # pre-order DFS: pivot trace and leaf sequence (divide.py:160-178)
+    trace, seq, stack = [], [], [0]
+    while stack:
+        q = stack.pop()
+        i_off, j_off, m, n, left, right, pi, pj, k, tot, lf = nodes[q]
+        if lf >= 0:
+            seq.append(lf)
+            cells += m * n
+            peak_table = max(peak_table, m * n)
+            continue
+        trace.append({"i": i_off + pi, "j": j_off + pj, "i_off": i_off, "j_off": j_off, "M": m, "N": n,
+                      "sub_i": pi, "sub_j": pj, "total_at_pivot": tot, "diagonal_k": k})
+        stack += [right, left]
+    parts = []
+    for s, lf in enumerate(seq):
+        i_off, j_off = nodes[leaves[lf]][:2]
+        p = got[lf] + np.array([i_off, j_off], np.int64)
+        parts.append(p if s == 0 else p[1:])
+    path = np.concatenate(parts, axis=0).astype(np.int64)
+    return AlignmentResult(
+        cost=engine.path_cost(path), path=path, cells_processed=int(cells), cells_budget=2 * M * N,
+        precision=str(dtype), algorithm="linmdtw", peak_diag_values=int(peak_diag),
+        peak_table_cells=int(peak_table), pivot_trace=tuple(trace),
+        level_stats=(("levels", nlevels), ("ranks", world)))

@@ -6,6 +6,7 @@ unfused, correctly rounded arithmetic, so no tolerance is needed)."""
 import numpy as np
 import pytest
 
+import bench
 import paper_2008_02734_b200 as L
 from golden_io import cases, tie_rule, trace_from
 from oracle import oracle as O
@@ -244,3 +245,51 @@ def test_linmdtw_matches_full_table_dtw_at_scale():
     assert np.array_equal(r.path, f.path)
     assert r.cost == f.cost
     assert 1.8 < r.cells_processed / (20000 * 18000) <= 2.0 + 1e-3
+
+
+def _dist_gpu_worker(rank, world, port, cases, q):
+    import os
+    import torch.distributed as dist
+    from paper_2008_02734_b200.distributed import linmdtw_distributed
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for M, N, d, seed, prec, min_dim in cases:
+            X, Y = bench.chroma_pair(M, N, d, seed=seed)
+            r = linmdtw_distributed(X, Y, min_dim=min_dim, precision=prec)
+            out.append((r.cost, r.path, r.cells_processed, r.peak_diag_values, r.peak_table_cells,
+                        list(r.pivot_trace)))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_device_engine_equals_single_gpu():
+    """Two ranks (gloo) sharing cuda:0 through the C ABI: top-level half passes
+    split across ranks, pivots combined on the host, leaves sharded; the
+    result equals the single-GPU engine's bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    cases = [(3000, 2600, 12, 7, 32, 500), (2200, 1800, 5, 8, 64, 300)]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_gpu_worker, args=(r, 2, port, cases, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for ci, (M, N, d, seed, prec, min_dim) in enumerate(cases):
+        X, Y = bench.chroma_pair(M, N, d, seed=seed)
+        ref = L.linmdtw(X, Y, min_dim=min_dim, precision=prec)
+        for rank in range(2):
+            cost, path, cells, pkd, pkt, trace = res[rank][ci]
+            assert cost == ref.cost and np.array_equal(path, ref.path)
+            assert cells == ref.cells_processed and pkd == ref.peak_diag_values and pkt == ref.peak_table_cells
+            assert trace == list(ref.pivot_trace)
