@@ -193,6 +193,22 @@ def cpu_desc():
     return model, os.cpu_count()
 
 
+def _bench_device() -> int:
+    if os.environ.get("LMDTW_BENCH_SAME_DEVICE") == "1":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def _allreduce(v: float, op: str) -> float:
+    """Scalar all-reduce over the bench ranks (device tensor under NCCL)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 # ------------------------------------------------------------------ arms
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU algorithm (the C oracle restating
@@ -235,13 +251,14 @@ def run_ours(args, rank, world):
     from paper_2008_02734_b200 import _capi
     from paper_2008_02734_b200.divide import _c_config
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = _bench_device()
     torch.cuda.set_device(dev)
     L.set_device(dev)
     lib = _capi.load()
     cfgd = CONFIGS[args.config]
     prec = cfgd["prec"]
     pairs = make_inputs(args.config)
+    n_total = len(pairs)
     d = pairs[0][0].shape[1]
     cfg = L.LinMdtwConfig(min_dim=args.min_dim, precision=prec)
     ccfg = _c_config(cfg)
@@ -252,8 +269,27 @@ def run_ours(args, rank, world):
     stream = torch.cuda.ExternalStream(_capi.stream_handle(dev))
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
+    # N > 1: one alignment's recursion sharded over the ranks (strong scaling,
+    # distributed.linmdtw_distributed); batches: pairs sharded longest-first
+    dist_single = world > 1 and len(pairs) == 1
+    if dist_single:
+        from paper_2008_02734_b200.distributed import DeviceEngine, linmdtw_distributed
+        resident = DeviceEngine(pairs[0][0], pairs[0][1], cfg, dev)
+    if world > 1 and len(pairs) > 1:
+        from paper_2008_02734_b200.distributed import lpt_assign
+        own = lpt_assign([X.shape[0] * Y.shape[0] for X, Y in pairs], world)
+        keep = [q for q in range(len(pairs)) if own[q] == rank]
+        pairs = [pairs[q] for q in keep]
+        dX = [dX[q] for q in keep]
+        dY = [dY[q] for q in keep]
+
     def one_device():
         n = len(pairs)
+        if dist_single:
+            r = linmdtw_distributed(pairs[0][0], pairs[0][1], config=cfg, engine=resident)
+            return r.cells_processed, None
+        if n == 0:
+            return 0, None
         if n == 1:
             h = C.c_void_p()
             _capi.check(lib.lmdtw_align(dev, C.c_void_p(dX[0].data_ptr()), pairs[0][0].shape[0],
@@ -306,10 +342,10 @@ def run_ours(args, rank, world):
     clocks = clk.summary()
     step_ms = sum(ms) / len(ms)
     if world > 1:
-        t = torch.tensor([step_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        step_ms = float(t.item())
-    value = (cells / args.steps) * world / (step_ms / 1e3) / 1e9
+        step_ms = _allreduce(step_ms, "max")
+        if not dist_single:  # sharded batch: every rank's pairs count
+            cells = int(_allreduce(float(cells), "sum"))
+    value = (cells / args.steps) / (step_ms / 1e3) / 1e9
 
     # e2e: the public drop-in API on pinned host buffers
     pin = []
@@ -319,6 +355,11 @@ def run_ours(args, rank, world):
         pin.append((L.FeatureSeries(tx.numpy()), L.FeatureSeries(ty.numpy()), tx, ty))
 
     def one_e2e():
+        if dist_single:
+            r = linmdtw_distributed(pin[0][0], pin[0][1], config=cfg)
+            return r.cells_processed, None
+        if len(pin) == 0:
+            return 0, None
         if len(pin) == 1:
             r = L.linmdtw(pin[0][0], pin[0][1], config=cfg)
             return r.cells_processed, None
@@ -328,7 +369,11 @@ def run_ours(args, rank, world):
     one_e2e()
     ems, ecells, _ = timed(one_e2e, max(1, min(args.steps, 3)))
     e2e_ms = sum(ems) / len(ems)
-    e2e_value = (ecells / len(ems)) * world / (e2e_ms / 1e3) / 1e9
+    if world > 1:
+        e2e_ms = _allreduce(e2e_ms, "max")
+        if not dist_single:
+            ecells = int(_allreduce(float(ecells), "sum"))
+    e2e_value = (ecells / len(ems)) / (e2e_ms / 1e3) / 1e9
     h2d = sum(X.nbytes + Y.nbytes for X, Y in pairs)
     K = sum(X.shape[0] + Y.shape[0] for X, Y in pairs)
     d2h = K * 16  # path (i,j) int64 pairs ~ M+N per alignment (upper bound)
@@ -355,11 +400,13 @@ def run_ours(args, rank, world):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": "strong" if dist_single else "weak", "vs_baseline": None,
         "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
         "config": {"workload": cfgd["workload"], "min_dim": args.min_dim, "precision": prec,
-                   "cells_per_step": cells // args.steps, "sec_per_alignment": round(step_ms / 1e3 / len(pairs), 6),
-                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": "single-gpu" if world == 1 else f"replicas{world}"},
+                   "cells_per_step": cells // args.steps, "sec_per_alignment": round(step_ms / 1e3 / n_total, 6),
+                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": ("single-gpu" if world == 1 else
+                                   (f"level-sharded x{world} (one alignment, distributed.py)" if dist_single
+                                    else f"pairs sharded longest-first over {world} ranks"))},
         "e2e": {"value": round(e2e_value, 3), "unit": "GCUPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
                 "api": "paper_2008_02734_b200.linmdtw (pinned host FeatureSeries)"},
@@ -399,8 +446,11 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(_bench_device())
+        # LMDTW_BENCH_BACKEND=gloo + LMDTW_BENCH_SAME_DEVICE=1: exercise the
+        # N > 1 path with every rank on cuda:0 (1-GPU boxes); timings then
+        # measure contention, not scaling
+        dist.init_process_group(os.environ.get("LMDTW_BENCH_BACKEND", "nccl"))
     run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist
