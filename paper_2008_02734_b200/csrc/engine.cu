@@ -879,6 +879,11 @@ void lmdtw_profile_get(double* out) {
     out[3] = g_stats.leaf_ms;
     out[4] = (double)g_stats.leaf_cells;
 }
+// Probe builds (LMDTW_WAITSTATS): blocked-wait cycles by tag (16 + 16 values).
+int lmdtw_debug_wait_stats(unsigned long long* cycles, unsigned long long* count, int reset) {
+    CU(wait_stats(cycles, count, reset));
+    return LMDTW_OK;
+}
 // The stream every kernel of `device` is launched on (for event timing).
 void* lmdtw_stream(int device) {
     Ctx* c = nullptr;

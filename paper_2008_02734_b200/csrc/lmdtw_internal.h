@@ -108,5 +108,6 @@ cudaError_t launch_pad_cast(int precision, const float* src, int64_t rows, int d
                             cudaStream_t stream);
 int max_resident_warps(int precision, int dp, int leaf, int device);
 cudaError_t set_watchdog_ns(unsigned long long ns);  // per device (current device)
+cudaError_t wait_stats(unsigned long long* cycles, unsigned long long* count, int reset);
 
 }  // namespace lmdtw

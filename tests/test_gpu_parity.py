@@ -247,6 +247,29 @@ def test_linmdtw_matches_full_table_dtw_at_scale():
     assert 1.8 < r.cells_processed / (20000 * 18000) <= 2.0 + 1e-3
 
 
+def test_cfg5_shape_skinny_fp64_vs_oracle():
+    """BASELINE cfg5's generator (random-walk latent, d=48, fp64, 10:1 aspect)
+    at 40k x 4k: path, cost, counters and pivot trace equal the oracle's;
+    the lopsided tree ends in skinny leaves."""
+    X, Y = bench.latent_pair(40000, 4000, 48, seed=5)
+    r = L.linmdtw(X, Y, precision=64)
+    o = O.linmdtw(X, Y, precision=64, nthreads=16)
+    assert_same_result(r, o)
+    assert max(t["M"] for t in r.pivot_trace) == 40000 and r.peak_table_cells > 0
+
+
+def test_cfg4_shape_batch_vs_oracle():
+    """BASELINE cfg4's shape (a batch of pairs with random lengths, chroma d=12,
+    fp32) scaled to lengths in [500, 3000]: every result of the fused batch
+    equals the oracle's single alignment."""
+    rng = np.random.default_rng(4)
+    MN = rng.integers(500, 3001, size=(12, 2))
+    pairs = [bench.chroma_pair(int(m), int(n), 12, seed=1000 + q) for q, (m, n) in enumerate(MN)]
+    batch = L.align_batch(pairs, precision=32)
+    for (X, Y), r in zip(pairs, batch):
+        assert_same_result(r, O.linmdtw(X, Y, precision=32, nthreads=16))
+
+
 def _dist_gpu_worker(rank, world, port, cases, q):
     import os
     import torch.distributed as dist
