@@ -111,29 +111,68 @@ def make_inputs(name):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    every 2 ms (pynvml), else nvidia-smi every 100 ms."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index=0):
         self.idx = gpu_index
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.source = "unsampled"
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+        while not self._stop.is_set():
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            self.mx.append(float(mx))
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            for nm, b in bits.items():
+                if r & b:
+                    self.reasons.add(nm)
+            self._stop.wait(0.002)
+
+    def _run_smi(self):
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
                 if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                    r = [x.strip() for x in out.split(",")]
+                    if r[1].replace(".", "").isdigit():
+                        self.sm.append(float(r[1]))
+                    if r[2].replace(".", "").isdigit():
+                        self.mx.append(float(r[2]))
+                    for q, nm in enumerate(self.NAMES):
+                        if len(r) > 5 + q and r[5 + q].lower().startswith("active"):
+                            self.reasons.add(nm)
             except Exception:
                 pass
             self._stop.wait(0.1)
+
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.source = "nvml"
+            try:
+                self._run_nvml(nv)
+            finally:
+                nv.nvmlShutdown()
+        except Exception:
+            self.source = "nvidia-smi"
+            self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -145,18 +184,10 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for q, nm in enumerate(names):
-                if len(r) > 5 + q and r[5 + q].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": self.source}
 
 
 # ------------------------------------------------------------------ helpers
