@@ -13,6 +13,7 @@
 // the reference's path_cost: per-cell costs summed sequentially in the
 // accumulation dtype (core.py:191-197).
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -318,6 +319,7 @@ struct Engine {
 
     int run_wave(const std::vector<PassDesc>& P0, int64_t bnd_total, bool leaf, void* tab, void* lcost,
                  int64_t cells) {
+        const auto th0 = std::chrono::steady_clock::now();
         // tile bookkeeping: per strip H+1 boundary values and a completion count
         std::vector<PassDesc> P(P0);
         int64_t lb_total = 0, flag_total = 0;
@@ -375,6 +377,9 @@ struct Engine {
             w.trace = c.trace.as<unsigned long long>();
         }
         const bool prof = g_profile.load() != 0;
+        if (getenv("LMDTW_HOST_TIMING"))
+            fprintf(stderr, "lmdtw host: %zu items prepared in %.1f us\n", items.size(),
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
         if (prof) CU(cudaEventRecord(c.ev0, c.st));
         TRY(launched(launch_wave(w, c.st), leaf ? "leaf wave_kernel" : "wave_kernel"));
         if (trace_file) {
@@ -484,7 +489,11 @@ struct Engine {
                      "pivot_kernel"));
         CU(cudaMemcpyAsync(c.h_pout.p, c.pout.p, V.size() * sizeof(PivotOut), cudaMemcpyDeviceToHost, c.st));
         c.d2h += V.size() * sizeof(PivotOut);
+        const auto ts0 = std::chrono::steady_clock::now();
         CU(cudaStreamSynchronize(c.st));
+        if (getenv("LMDTW_HOST_TIMING"))
+            fprintf(stderr, "lmdtw host: level waited %.1f us for the device\n",
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts0).count());
         const PivotOut* po = c.h_pout.as<PivotOut>();
         for (size_t q = 0; q < nodes.size(); q++) {
             Node& n = all[nodes[q]];
