@@ -297,21 +297,21 @@ struct Engine {
         constexpr int64_t kPer = kTileW / kLagKey;
         int64_t mmax = 0, total = 0;
         for (const auto& p : P)
-            for (int a = 0; a < p.nstrips; a++) {
+            for (int a = p.strip_lo; a < p.strip_hi; a++) {
                 const int64_t nb = tiles_of(p, a, H);
                 mmax = std::max<int64_t>(mmax, (nb - 1) * kPer + a);
                 total += nb;
             }
         std::vector<int64_t> cnt(mmax + 2, 0);
         for (const auto& p : P)
-            for (int a = 0; a < p.nstrips; a++) {
+            for (int a = p.strip_lo; a < p.strip_hi; a++) {
                 const int64_t nb = tiles_of(p, a, H);
                 for (int64_t b = 0; b < nb; b++) cnt[b * kPer + a + 1]++;
             }
         for (int64_t m = 1; m <= mmax + 1; m++) cnt[m] += cnt[m - 1];
         items.resize(total);
         for (size_t q = 0; q < P.size(); q++)
-            for (int a = 0; a < P[q].nstrips; a++) {
+            for (int a = P[q].strip_lo; a < P[q].strip_hi; a++) {
                 const int64_t nb = tiles_of(P[q], a, H);
                 for (int64_t b = 0; b < nb; b++) items[cnt[b * kPer + a]++] = WorkItem{(int)q, a, (int)b, 0};
             }
@@ -434,6 +434,9 @@ struct Engine {
         }
         p.bnd_off = bnd_total;
         bnd_total += 2 * ((N + 1) & ~1LL) * bwords();  // two slots, 16-byte aligned
+        p.strip_lo = 0;
+        p.strip_hi = p.nstrips;
+        p.bnd_in_first = 0;
         p.bp_off = 0;
         p.tab_off = -1;
         p.w64 = 0;
@@ -527,6 +530,9 @@ struct Engine {
             p.reverse = 0;
             p.rows = (int32_t)nd.M;
             p.nstrips = (p.rows + H - 1) / H;
+            p.strip_lo = 0;
+            p.strip_hi = p.nstrips;
+            p.bnd_in_first = 0;
             p.bnd_off = bnd_total;
             bnd_total += 2 * ((nd.N + 1) & ~1LL) * bwords();  // two slots, 16-byte aligned
             p.w64 = (int32_t)((nd.N + 31) / 32);
@@ -944,6 +950,132 @@ int lmdtw_debug_wave_independent(int device, int32_t precision, int32_t d, int32
     tot = f;
     *ms = tot / reps;
     return LMDTW_OK;
+}
+
+// Test hook for strip sharding (not part of the reference-facing ABI): one
+// half pass split into `nshards` contiguous strip ranges, each run by its own
+// persistent wave kernel on its own stream and buffers, concurrently on one
+// GPU; shard s reads the boundary row of shard s-1's last strip from shard
+// s-1's handoff buffer (what a peer GPU's buffer is in the multi-GPU layout).
+// The outputs are merged by row range into the host buffers of diag_dtw.
+int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d,
+                                  int64_t kstop, int32_t reverse, int32_t precision, int32_t nshards, void* out_d[3],
+                                  void* out_c[3]) {
+    TRY(validate_common(M, N, d, precision));
+    if (kstop < 2 || kstop > M + N - 2) return set_err(LMDTW_EINVAL, "kstop out of range [2, M+N-2]");
+    if (nshards < 1) return set_err(LMDTW_EINVAL, "nshards must be >= 1");
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    Engine E(*c, precision, d);
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&X, &M, 1, LMDTW_MEM_HOST, true, xb));
+    TRY(E.stage(&Y, &N, 1, LMDTW_MEM_HOST, false, yb));
+    CU(cudaStreamSynchronize(c->st));
+    int64_t out_total = 0, bnd_total = 0;
+    const PassDesc base = E.half_pass_desc(xb[0], yb[0], M, N, kstop, reverse ? 1 : 0, out_total, bnd_total);
+    const int S = base.nstrips, H = E.H;
+    const int ns = std::min<int>(nshards, S);
+    // contiguous strip ranges of about equal cell counts
+    std::vector<int64_t> scells(S);
+    int64_t all = 0;
+    for (int a = 0; a < S; a++) {
+        const int64_t r0 = (int64_t)a * H, r1 = std::min<int64_t>(base.rows, r0 + H);
+        scells[a] = cells_upto(kstop, r1, N) - cells_upto(kstop, r0, N);
+        all += scells[a];
+    }
+    std::vector<int> lo(ns + 1, S);
+    lo[0] = 0;
+    int64_t acc = 0;
+    for (int a = 0, sh = 1; a < S && sh < ns; a++) {
+        acc += scells[a];
+        if (acc * ns >= all * sh && S - (a + 1) >= ns - sh) lo[sh++] = a + 1;
+    }
+    struct Shard {
+        PassDesc pd;
+        std::vector<WorkItem> items;
+        DBuf passes, items_d, counter, bnd, lb, flags, out;
+        cudaStream_t st = nullptr;
+    };
+    std::vector<Shard> sh(ns);
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    int rc = LMDTW_OK;
+    for (int q = 0; q < ns && rc == LMDTW_OK; q++) {
+        Shard& z = sh[q];
+        z.pd = base;
+        z.pd.strip_lo = lo[q];
+        z.pd.strip_hi = lo[q + 1];
+        z.pd.tile_w = kTileW;
+        z.pd.lb_off = 0;
+        z.pd.flag_off = 0;
+        E.make_items(std::vector<PassDesc>{z.pd}, z.items);
+        if (z.bnd.ensure((size_t)bnd_total * 8) != cudaSuccess || z.out.ensure((size_t)out_total * E.esz) ||
+            z.passes.ensure(sizeof(PassDesc)) || z.items_d.ensure(z.items.size() * sizeof(WorkItem)) ||
+            z.counter.ensure(sizeof(int)) || z.lb.ensure((size_t)S * (H + 1) * E.esz) ||
+            z.flags.ensure((size_t)S * sizeof(int)) || cudaStreamCreateWithFlags(&z.st, cudaStreamNonBlocking))
+            rc = set_err(LMDTW_ENOMEM, "sharded half pass: allocation failed");
+    }
+    if (rc == LMDTW_OK) {
+        for (int q = 0; q < ns; q++) {
+            Shard& z = sh[q];
+            z.pd.bnd_in_first = q > 0 ? (uint64_t)(uintptr_t)sh[q - 1].bnd.p : 0;
+            cudaMemcpy(z.passes.p, &z.pd, sizeof(PassDesc), cudaMemcpyHostToDevice);
+            cudaMemcpy(z.items_d.p, z.items.data(), z.items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice);
+            cudaMemset(z.counter.p, 0, sizeof(int));
+            cudaMemset(z.bnd.p, 0xFF, (size_t)bnd_total * 8);  // tag -1
+            cudaMemset(z.flags.p, 0, (size_t)S * sizeof(int));
+        }
+        CU(cudaDeviceSynchronize());  // every buffer initialised before any shard runs
+        for (int q = 0; q < ns; q++) {
+            Shard& z = sh[q];
+            WaveLaunch w{};
+            w.X = c->xp.p;
+            w.Y = c->yp.p;
+            w.dp = E.dp;
+            w.precision = precision;
+            w.passes = z.passes.as<PassDesc>();
+            w.items = z.items_d.as<WorkItem>();
+            w.nitems = (int)z.items.size();
+            w.counter = z.counter.as<int>();
+            w.out = z.out.p;
+            w.bnd = z.bnd.p;
+            w.lb = z.lb.p;
+            w.flags = z.flags.as<int>();
+            w.tie0 = 2;
+            w.tie1 = 0;
+            w.tie2 = 1;
+            w.grid_warps = std::max(1, nsm / ns);  // CTAs: the shards share the SMs
+            CU(launch_wave(w, z.st));
+        }
+        CU(cudaDeviceSynchronize());
+        // merge the last three diagonals by row range: idx = min(k, M-1) - i
+        for (int s3 = 0; s3 < 3; s3++) {
+            const int64_t k = kstop - 2 + s3, L = dlen(k, M, N);
+            if (L <= 0) continue;
+            const int64_t top = std::min<int64_t>(k, M - 1), ilo = std::max<int64_t>(0, k - (N - 1));
+            for (int q = 0; q < ns; q++) {
+                const int64_t r0 = std::max<int64_t>((int64_t)lo[q] * H, ilo);
+                const int64_t r1 = std::min<int64_t>((int64_t)lo[q + 1] * H - 1, top);
+                if (r1 < r0) continue;
+                const int64_t i0 = top - r1, cnt = r1 - r0 + 1;
+                if (out_d && out_d[s3])
+                    CU(cudaMemcpy((char*)out_d[s3] + i0 * E.esz, (char*)sh[q].out.p + (base.out_off[s3] + i0) * E.esz,
+                                  cnt * E.esz, cudaMemcpyDeviceToHost));
+                if (out_c && out_c[s3])
+                    CU(cudaMemcpy((char*)out_c[s3] + i0 * E.esz,
+                                  (char*)sh[q].out.p + (base.out_off[3 + s3] + i0) * E.esz, cnt * E.esz,
+                                  cudaMemcpyDeviceToHost));
+            }
+        }
+    }
+    for (auto& z : sh) {
+        if (z.st) cudaStreamDestroy(z.st);
+        for (DBuf* b : {&z.passes, &z.items_d, &z.counter, &z.bnd, &z.lb, &z.flags, &z.out})
+            if (b->p) cudaFree(b->p);
+    }
+    return rc;
 }
 
 int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d, int64_t kstop,

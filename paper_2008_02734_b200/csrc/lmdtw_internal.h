@@ -28,7 +28,11 @@ struct PassDesc {
     int64_t lb_off;         // tile left boundaries: nstrips x (H + 1) values (set by the launcher)
     int64_t flag_off;       // tiles completed per strip: nstrips ints (set by the launcher)
     int32_t tile_w;         // columns per tile (set by the launcher)
+    int32_t strip_lo;       // strips [strip_lo, strip_hi) run in this launch (a shard of the pass)
+    int32_t strip_hi;
     int32_t pad;
+    uint64_t bnd_in_first;  // != 0: strip strip_lo reads strip strip_lo-1's handoff slots here
+                            // (another shard's buffer, e.g. a peer GPU's), system-scope loads
 };
 
 // Columns per work item: a strip is cut into tiles of kTileW columns so the

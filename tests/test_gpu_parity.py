@@ -316,3 +316,34 @@ def test_distributed_device_engine_equals_single_gpu():
             assert cost == ref.cost and np.array_equal(path, ref.path)
             assert cells == ref.cells_processed and pkd == ref.peak_diag_values and pkt == ref.peak_table_cells
             assert trace == list(ref.pivot_trace)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("reverse", [0, 1])
+def test_strip_sharded_half_pass_equals_unsharded(prec, reverse):
+    """The strip-sharding mechanism of the multi-GPU layout, on one GPU: a half
+    pass split into 2-4 contiguous strip ranges, each a separate persistent
+    kernel on its own stream and buffers running concurrently, the first strip
+    of every range reading the previous range's handoff buffer with
+    system-scope loads.  The merged last three diagonals equal the unsharded
+    pass bit for bit."""
+    import ctypes as C
+    from paper_2008_02734_b200 import _capi
+    lib = _capi.load()
+    dt = np.float32 if prec == 32 else np.float64
+    for (M, N, d, kfrac, seed) in [(1500, 5200, 12, 0.5, 1), (2100, 4300, 3, 0.8, 2), (900, 2500, 12, 1.0, 3)]:
+        X, Y = bench.chroma_pair(M, N, d, seed=seed)
+        kstop = max(2, min(M + N - 2, int(kfrac * (M + N - 2))))
+        lens = [L.diag_length(kstop - 2 + s, M, N) for s in range(3)]
+        ref = L.diag_dtw(X, Y, kstop, "reverse" if reverse else "forward", precision=prec)
+        for ns in (2, 3, 4):
+            od = [np.full(max(n, 1), np.nan, dt) for n in lens]
+            oc = [np.full(max(n, 1), np.nan, dt) for n in lens]
+            pd = (C.c_void_p * 3)(*[o.ctypes.data for o in od])
+            pc = (C.c_void_p * 3)(*[o.ctypes.data for o in oc])
+            _capi.check(lib.lmdtw_debug_sharded_half_pass(
+                0, _capi.ptr(X), C.c_int64(M), _capi.ptr(Y), C.c_int64(N), d, C.c_int64(kstop), reverse, prec, ns,
+                pd, pc))
+            for s in range(3):
+                assert np.array_equal(od[s][:lens[s]], ref.d[s]), (M, N, ns, s)
+                assert np.array_equal(oc[s][:lens[s]], ref.c[s]), (M, N, ns, s)
