@@ -165,6 +165,30 @@ int lmdtw_pivot_combine(int32_t precision, int64_t M, int64_t N, int32_t pivot_h
                         const void *const fwd_d[3], const void *const fwd_c[3],
                         const void *const bwd_d[3], int64_t *ijk, double *total);
 
+/* One shard of a half pass for the multi-GPU layout: strips
+ * [strip_lo, strip_hi) of diag_dtw(X, Y, kstop, reverse), strips being
+ * lmdtw_strip_height() grid rows.  bnd_local: caller-owned device buffer of
+ * lmdtw_handoff_words(N) 64-bit words, set to all ones before ANY shard of the
+ * pass starts; this shard's strips publish their bottom rows there.  bnd_prev:
+ * the previous shard's bnd_local (a peer GPU's memory mapped with CUDA IPC),
+ * NULL for strip_lo = 0; read with system-scope loads.  The entries of the last
+ * three diagonals that belong to rows [strip_lo H, strip_hi H) are written to
+ * the host buffers (other entries untouched); *cells = the shard's cells. */
+int lmdtw_half_pass_shard(int device, const float *X, int64_t M, const float *Y, int64_t N, int32_t d,
+                          int64_t kstop, int32_t reverse, int32_t precision, int32_t mem, int32_t strip_lo,
+                          int32_t strip_hi, void *bnd_local, const void *bnd_prev, void *out_d[3],
+                          void *out_c[3], int64_t *cells);
+int64_t lmdtw_handoff_words(int64_t N, int32_t precision);
+/* Handoff buffers shared between the processes of a sharded pass (CUDA IPC):
+ * allocate + export a 64-byte handle, open a peer's handle (peer access
+ * enabled), close, free, and set every byte to 0xFF (synchronously). */
+int lmdtw_ipc_alloc(int device, int64_t bytes, void **ptr, unsigned char handle[64]);
+int lmdtw_ipc_open(int device, const unsigned char handle[64], void **ptr);
+int lmdtw_ipc_close(int device, void *ptr);
+int lmdtw_ipc_free(int device, void *ptr);
+int lmdtw_fill_ones(int device, void *ptr, int64_t bytes);
+int32_t lmdtw_strip_height(int32_t precision, int32_t d);
+
 int lmdtw_result_info(const lmdtw_result_t *r, lmdtw_align_info_t *info);
 /* Copies K (i,j) int64 pairs. */
 int lmdtw_result_path(const lmdtw_result_t *r, int64_t *path_out);

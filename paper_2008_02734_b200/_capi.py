@@ -45,7 +45,8 @@ EXPORTS = (
     "lmdtw_align_batch", "lmdtw_result_info", "lmdtw_result_path", "lmdtw_result_pivots",
     "lmdtw_result_free", "lmdtw_path_cost", "lmdtw_diag_length", "lmdtw_cells_upto",
     "lmdtw_peak_retained_values", "lmdtw_launch_count", "lmdtw_pivot_nodes", "lmdtw_leaf_nodes",
-    "lmdtw_pivot_combine",
+    "lmdtw_pivot_combine", "lmdtw_half_pass_shard", "lmdtw_handoff_words", "lmdtw_strip_height",
+    "lmdtw_ipc_alloc", "lmdtw_ipc_open", "lmdtw_ipc_close", "lmdtw_ipc_free", "lmdtw_fill_ones",
 )
 
 _lib = None
@@ -58,7 +59,7 @@ def load():
         return _lib
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2008_02734_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2008_02734_b200/build.py` "
             "(there is no CPU fallback)")
     L = C.CDLL(LIB_PATH)
     P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -91,6 +92,17 @@ def load():
     L.lmdtw_leaf_nodes.argtypes = [C.c_int, P, I64, P, I64, I32, I32, P, P, I32, I32, P, P]
     L.lmdtw_leaf_nodes.restype = C.c_int
     L.lmdtw_pivot_combine.argtypes = [I32, I64, I64, I32, P, P, P, P, P]
+    L.lmdtw_half_pass_shard.argtypes = [C.c_int, P, I64, P, I64, I32, I64, I32, I32, I32, I32, I32, P, P, P, P, P]
+    L.lmdtw_half_pass_shard.restype = C.c_int
+    L.lmdtw_handoff_words.argtypes = [I64, I32]
+    L.lmdtw_handoff_words.restype = I64
+    L.lmdtw_strip_height.argtypes = [I32, I32]
+    L.lmdtw_strip_height.restype = I32
+    L.lmdtw_ipc_alloc.argtypes = [C.c_int, I64, P, P]
+    L.lmdtw_ipc_open.argtypes = [C.c_int, P, P]
+    L.lmdtw_ipc_close.argtypes = [C.c_int, P]
+    L.lmdtw_ipc_free.argtypes = [C.c_int, P]
+    L.lmdtw_fill_ones.argtypes = [C.c_int, P, I64]
     L.lmdtw_pivot_combine.restype = C.c_int
     L.lmdtw_path_cost.argtypes = [P, I64, P, I64, I32, P, I64, I32, P]
     L.lmdtw_path_cost.restype = C.c_int

@@ -1,6 +1,7 @@
 """Build liblmdtw_b200.so in-tree with nvcc for sm_100a.
 
-    python -m paper_2008_02734_b200.build [--force]
+    python paper_2008_02734_b200/build.py [--force]   (a script: importing the
+    package needs a current library, building must not)
 
 The shared library lands next to this file so it travels with the repo
 snapshot to the GPU box (it is git-ignored, not gpurun-ignored).

@@ -952,6 +952,134 @@ int lmdtw_debug_wave_independent(int device, int32_t precision, int32_t d, int32
     return LMDTW_OK;
 }
 
+int64_t lmdtw_handoff_words(int64_t N, int32_t precision) { return 2 * ((N + 1) & ~1LL) * (precision == 32 ? 1 : 2); }
+
+int32_t lmdtw_strip_height(int32_t precision, int32_t d) {
+    const int dp = supported_dp(precision, d);
+    return dp < 0 ? -1 : strip_height(precision, dp);
+}
+
+int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d, int64_t kstop,
+                          int32_t reverse, int32_t precision, int32_t mem, int32_t strip_lo, int32_t strip_hi,
+                          void* bnd_local, const void* bnd_prev, void* out_d[3], void* out_c[3], int64_t* cells) {
+    TRY(validate_common(M, N, d, precision));
+    if (kstop < 2 || kstop > M + N - 2) return set_err(LMDTW_EINVAL, "kstop out of range [2, M+N-2]");
+    if (!bnd_local) return set_err(LMDTW_EINVAL, "bnd_local is required");
+    Ctx* c = nullptr;
+    TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    c->call_launches = 0;
+    Engine E(*c, precision, d);
+    std::vector<int64_t> xb, yb;
+    TRY(E.stage(&X, &M, 1, mem, true, xb));
+    TRY(E.stage(&Y, &N, 1, mem, false, yb));
+    int64_t out_total = 0, bnd_total = 0;
+    PassDesc pd = E.half_pass_desc(xb[0], yb[0], M, N, kstop, reverse ? 1 : 0, out_total, bnd_total);
+    if (strip_lo < 0 || strip_hi > pd.nstrips || strip_lo >= strip_hi)
+        return set_err(LMDTW_EINVAL, "strip range outside the pass");
+    if (strip_lo > 0 && !bnd_prev) return set_err(LMDTW_EINVAL, "bnd_prev is required after the first shard");
+    const int H = E.H;
+    pd.strip_lo = strip_lo;
+    pd.strip_hi = strip_hi;
+    pd.tile_w = kTileW;
+    pd.lb_off = 0;
+    pd.flag_off = 0;
+    pd.bnd_off = 0;
+    pd.bnd_in_first = strip_lo > 0 ? (uint64_t)(uintptr_t)bnd_prev : 0;
+    std::vector<WorkItem> items;
+    E.make_items(std::vector<PassDesc>{pd}, items);
+    CU(c->out.ensure((size_t)out_total * E.esz));
+    CU(c->passes.ensure(sizeof(PassDesc)));
+    CU(c->items.ensure(items.size() * sizeof(WorkItem)));
+    CU(c->counter.ensure(sizeof(int)));
+    CU(c->lb.ensure((size_t)pd.nstrips * (H + 1) * E.esz));
+    CU(c->flags.ensure((size_t)pd.nstrips * sizeof(int)));
+    CU(c->h_passes.ensure(sizeof(PassDesc)));
+    CU(c->h_items.ensure(items.size() * sizeof(WorkItem)));
+    memcpy(c->h_passes.p, &pd, sizeof(PassDesc));
+    memcpy(c->h_items.p, items.data(), items.size() * sizeof(WorkItem));
+    CU(cudaMemcpyAsync(c->passes.p, c->h_passes.p, sizeof(PassDesc), cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->items.p, c->h_items.p, items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
+    CU(cudaMemsetAsync(c->flags.p, 0, (size_t)pd.nstrips * sizeof(int), c->st));
+    WaveLaunch w{};
+    w.X = c->xp.p;
+    w.Y = c->yp.p;
+    w.dp = E.dp;
+    w.precision = precision;
+    w.passes = c->passes.as<PassDesc>();
+    w.items = c->items.as<WorkItem>();
+    w.nitems = (int)items.size();
+    w.counter = c->counter.as<int>();
+    w.out = c->out.p;
+    w.bnd = bnd_local;
+    w.lb = c->lb.p;
+    w.flags = c->flags.as<int>();
+    w.tie0 = 2;
+    w.tie1 = 0;
+    w.tie2 = 1;
+    TRY(E.launched(launch_wave(w, c->st), "wave_kernel (shard)"));
+    // the shard's rows of the last three diagonals: idx = min(k, M-1) - i
+    for (int s3 = 0; s3 < 3; s3++) {
+        const int64_t k = kstop - 2 + s3, L = dlen(k, M, N);
+        if (L <= 0) continue;
+        const int64_t top = std::min<int64_t>(k, M - 1), ilo = std::max<int64_t>(0, k - (N - 1));
+        const int64_t r0 = std::max<int64_t>((int64_t)strip_lo * H, ilo);
+        const int64_t r1 = std::min<int64_t>((int64_t)strip_hi * H - 1, top);
+        if (r1 < r0) continue;
+        const int64_t i0 = top - r1, cnt = r1 - r0 + 1;
+        if (out_d && out_d[s3])
+            CU(cudaMemcpyAsync((char*)out_d[s3] + i0 * E.esz, (char*)c->out.p + (pd.out_off[s3] + i0) * E.esz,
+                               cnt * E.esz, cudaMemcpyDeviceToHost, c->st));
+        if (out_c && out_c[s3])
+            CU(cudaMemcpyAsync((char*)out_c[s3] + i0 * E.esz, (char*)c->out.p + (pd.out_off[3 + s3] + i0) * E.esz,
+                               cnt * E.esz, cudaMemcpyDeviceToHost, c->st));
+    }
+    CU(cudaStreamSynchronize(c->st));
+    if (cells) {
+        const int64_t ra = (int64_t)strip_lo * H, rb = std::min<int64_t>(pd.rows, (int64_t)strip_hi * H);
+        *cells = cells_upto(kstop, rb, N) - cells_upto(kstop, ra, N);
+    }
+    return LMDTW_OK;
+}
+
+// Handoff buffers shared between the ranks of a sharded pass (CUDA IPC).
+int lmdtw_ipc_alloc(int device, int64_t bytes, void** ptr, unsigned char handle[64]) {
+    if (!ptr || !handle || bytes <= 0) return set_err(LMDTW_EINVAL, "bad ipc allocation request");
+    CU(cudaSetDevice(device));
+    CU(cudaMalloc(ptr, (size_t)bytes));
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, *ptr));
+    memcpy(handle, &h, 64);
+    return LMDTW_OK;
+}
+int lmdtw_ipc_open(int device, const unsigned char handle[64], void** ptr) {
+    if (!ptr || !handle) return set_err(LMDTW_EINVAL, "bad ipc handle");
+    CU(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    CU(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return LMDTW_OK;
+}
+int lmdtw_ipc_close(int device, void* ptr) {
+    CU(cudaSetDevice(device));
+    CU(cudaIpcCloseMemHandle(ptr));
+    return LMDTW_OK;
+}
+int lmdtw_ipc_free(int device, void* ptr) {
+    CU(cudaSetDevice(device));
+    CU(cudaFree(ptr));
+    return LMDTW_OK;
+}
+// All bytes 0xFF (handoff tag -1), synchronously.
+int lmdtw_fill_ones(int device, void* ptr, int64_t bytes) {
+    CU(cudaSetDevice(device));
+    CU(cudaMemset(ptr, 0xFF, (size_t)bytes));
+    CU(cudaDeviceSynchronize());
+    return LMDTW_OK;
+}
+
 // Test hook for strip sharding (not part of the reference-facing ABI): one
 // half pass split into `nshards` contiguous strip ranges, each run by its own
 // persistent wave kernel on its own stream and buffers, concurrently on one

@@ -10,8 +10,13 @@ level on every rank with identical bookkeeping; only the compute is split:
   (lmdtw_pivot_nodes) and the pivots are exchanged (all_gather).
 * A level with fewer nodes than ranks (the top of the tree: one node at
   level 0) is split one step further, into the nodes' forward and reverse
-  half passes (diagonal.diag_dtw, diagonal.py:172-223), again assigned
-  longest-first.  The owners exchange the three returned diagonals and every
+  half passes (diagonal.diag_dtw, diagonal.py:172-223).  With at least as
+  many half passes as ranks they are assigned longest-first; with fewer, each
+  half pass gets a group of ranks and is cut into contiguous strip ranges
+  (shards): every shard runs as its own persistent kernel and its first strip
+  reads the previous shard's boundary row straight from that rank's GPU
+  memory (CUDA IPC handle, NVLink peer access, lmdtw_half_pass_shard) while
+  both run.  The owners exchange the three returned diagonals and every
   rank applies the split-point combine of divide.find_pivot
   (divide.py:122-145; lmdtw_pivot_combine) to the same data.
 * Leaves (divide.py:153-157) are sharded the same way; their paths are
@@ -67,6 +72,47 @@ def _kstops(M, N):
     return kf, kb
 
 
+def apportion(world, weights):
+    """Ranks per unit, proportional to weight, at least one each (len(weights) <= world)."""
+    n = len(weights)
+    alloc = [1] * n
+    for _ in range(world - n):
+        q = max(range(n), key=lambda q: (weights[q] / alloc[q], -q))
+        alloc[q] += 1
+    return alloc
+
+
+def strip_ranges(kstop, M, N, H, parts):
+    """Contiguous strip ranges [lo, hi) of one half pass with about equal cells."""
+    rows = min(M, kstop + 1)
+    S = (rows + H - 1) // H
+    parts = max(1, min(parts, S))
+    cells = [_cells_upto(kstop, min(rows, (a + 1) * H), N) - _cells_upto(kstop, a * H, N) for a in range(S)]
+    total = sum(cells)
+    bounds, acc, k = [0], 0, 1
+    for a in range(S):
+        acc += cells[a]
+        if k < parts and acc * parts >= total * k and S - (a + 1) >= parts - k:
+            bounds.append(a + 1)
+            k += 1
+    while len(bounds) < parts:  # degenerate tails
+        bounds.append(bounds[-1])
+    bounds.append(S)
+    return [(bounds[q], bounds[q + 1]) for q in range(parts)]
+
+
+def _shard_idx(kstop, M, N, lo, hi, H):
+    """Index range [a, b) of each of the last three diagonals owned by rows
+    [lo H, hi H) (idx = min(k, M-1) - i, diagonal.py:36-41)."""
+    out = []
+    for s3 in range(3):
+        k = kstop - 2 + s3
+        top, ilo = min(k, M - 1), max(0, k - (N - 1))
+        r0, r1 = max(lo * H, ilo), min(hi * H - 1, top)
+        out.append((top - r1, top - r0 + 1) if r1 >= r0 else (0, 0))
+    return out
+
+
 class DeviceEngine:
     """This rank's compute through the C ABI, features resident on its GPU."""
 
@@ -120,6 +166,54 @@ class DeviceEngine:
             1 if reverse else 0, self.prec, _capi.MEM_DEVICE, pd, pc, C.byref(cells)))
         return [d[s][:lens[s]] for s in range(3)], [c[s][:lens[s]] for s in range(3)]
 
+    def strip_height(self):
+        return int(self.lib.lmdtw_strip_height(self.prec, self.d))
+
+    def half_pass_shard(self, sub, reverse, lo, hi, bnd_local, bnd_prev):
+        """Strips [lo, hi) of one half pass (lmdtw_half_pass_shard): returns
+        {slot: (first idx, D segment, C segment)} for this shard's rows."""
+        i_off, j_off, M, N = sub
+        kf, kb = _kstops(M, N)
+        kstop = kb if reverse else kf
+        dt = np.float32 if self.prec == 32 else np.float64
+        lens = [int(self.lib.lmdtw_diag_length(kstop - 2 + s, M, N)) for s in range(3)]
+        d = [np.empty(max(L, 1), dt) for L in lens]
+        c = [np.empty(max(L, 1), dt) for L in lens]
+        pd = (C.c_void_p * 3)(*[a.ctypes.data for a in d])
+        pc = (C.c_void_p * 3)(*[a.ctypes.data for a in c])
+        cells = C.c_int64()
+        Xs = self.Xd[i_off:i_off + M]
+        Ys = self.Yd[j_off:j_off + N]
+        _capi.check(self.lib.lmdtw_half_pass_shard(
+            self.device, C.c_void_p(Xs.data_ptr()), M, C.c_void_p(Ys.data_ptr()), N, self.d, kstop,
+            1 if reverse else 0, self.prec, _capi.MEM_DEVICE, lo, hi, bnd_local, bnd_prev, pd, pc, C.byref(cells)))
+        out = {}
+        for s3, (a, b) in enumerate(_shard_idx(kstop, M, N, lo, hi, self.strip_height())):
+            if b > a:
+                out[s3] = (a, d[s3][a:b].copy(), c[s3][a:b].copy())
+        return out
+
+    def handoff_alloc(self, nbytes):
+        ptr = C.c_void_p()
+        h = (C.c_ubyte * 64)()
+        _capi.check(self.lib.lmdtw_ipc_alloc(self.device, int(nbytes), C.byref(ptr), h))
+        return ptr, bytes(h)
+
+    def handoff_open(self, handle):
+        ptr = C.c_void_p()
+        h = (C.c_ubyte * 64).from_buffer_copy(handle)
+        _capi.check(self.lib.lmdtw_ipc_open(self.device, h, C.byref(ptr)))
+        return ptr
+
+    def handoff_reset(self, ptr, nbytes):
+        _capi.check(self.lib.lmdtw_fill_ones(self.device, ptr, int(nbytes)))
+
+    def handoff_close(self, ptr):
+        _capi.check(self.lib.lmdtw_ipc_close(self.device, ptr))
+
+    def handoff_free(self, ptr):
+        _capi.check(self.lib.lmdtw_ipc_free(self.device, ptr))
+
     def combine(self, M, N, fwd_d, fwd_c, bwd_d):
         """Split point from the two halves (divide.py:122-145)."""
         fd = (C.c_void_p * 3)(*[np.ascontiguousarray(a).ctypes.data for a in fwd_d])
@@ -165,6 +259,65 @@ def _all_gather(obj, group):
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, obj, group=group)
     return out
+
+
+def _sharded_half_passes(engine, subs, units, weights, rank, world, group):
+    """Fewer half passes than ranks: each gets a group of consecutive ranks and
+    is cut into strip shards that run concurrently, shard j's first strip
+    reading shard j-1's handoff buffer through CUDA IPC.  Returns
+    {unit: (d[3], c[3])} with the merged diagonals, on every rank."""
+    import torch.distributed as dist
+    H = engine.strip_height()
+    alloc = apportion(world, weights)
+    plan, r = {}, 0  # rank -> (unit, shard index, lo, hi)
+    shards_of = {}
+    for u, g in enumerate(alloc):
+        q, rev = units[u]
+        _, _, m, n = subs[q]
+        kstop = _kstops(m, n)[rev]
+        rngs = strip_ranges(kstop, m, n, H, g)
+        shards_of[u] = []
+        for j in range(g):
+            if j < len(rngs) and rngs[j][1] > rngs[j][0]:
+                plan[r] = (u, j, rngs[j][0], rngs[j][1])
+                shards_of[u].append(r)
+            r += 1
+    nmax = max(n for _, _, _, n in subs)
+    nbytes = int(_capi.load().lmdtw_handoff_words(nmax, engine.prec)) * 8
+    ptr, handle = engine.handoff_alloc(nbytes)
+    handles = _all_gather(handle, group)
+    engine.handoff_reset(ptr, nbytes)
+    dist.barrier(group)  # every buffer reads tag -1 before any shard runs
+    peer = None
+    out = {}
+    try:
+        if rank in plan:
+            u, j, lo, hi = plan[rank]
+            prev = None
+            if j > 0:
+                peer = engine.handoff_open(handles[shards_of[u][j - 1]])
+                prev = peer
+            out = {u: engine.half_pass_shard(subs[units[u][0]], units[u][1], lo, hi, ptr, prev)}
+        parts = _all_gather(out, group)
+    finally:
+        dist.barrier(group)  # no shard still reads a peer buffer
+        if peer is not None:
+            engine.handoff_close(peer)
+        engine.handoff_free(ptr)
+    got = {}
+    dt = np.float32 if engine.prec == 32 else np.float64
+    for u, (q, rev) in enumerate(units):
+        _, _, m, n = subs[q]
+        kstop = _kstops(m, n)[rev]
+        lens = [int(_capi.load().lmdtw_diag_length(kstop - 2 + s3, m, n)) for s3 in range(3)]
+        d = [np.full(L, np.nan, dt) for L in lens]
+        c = [np.full(L, np.nan, dt) for L in lens]
+        for part in parts:
+            for s3, (a, sd, sc) in part.get(u, {}).items():
+                d[s3][a:a + len(sd)] = sd
+                c[s3][a:a + len(sc)] = sc
+        got[u] = (d, c)
+    return got
 
 
 def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | None = None, group=None,
@@ -218,12 +371,15 @@ def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | N
             # forward and reverse half passes as separate units
             units = [(q, rev) for q in range(len(subs)) for rev in (0, 1)]
             w = [_cells_upto(_kstops(*subs[q][2:])[rev], *subs[q][2:]) for q, rev in units]
-            owner = lpt_assign(w, world)
-            mine = [u for u in range(len(units)) if owner[u] == rank]
-            res = {u: engine.half_pass(subs[units[u][0]], units[u][1]) for u in mine}
-            got = {}
-            for part in _all_gather(res, group):
-                got.update(part)
+            if len(units) >= world or not hasattr(engine, "half_pass_shard"):
+                owner = lpt_assign(w, world)
+                mine = [u for u in range(len(units)) if owner[u] == rank]
+                res = {u: engine.half_pass(subs[units[u][0]], units[u][1]) for u in mine}
+                got = {}
+                for part in _all_gather(res, group):
+                    got.update(part)
+            else:
+                got = _sharded_half_passes(engine, subs, units, w, rank, world, group)
             piv = []
             for q in range(len(subs)):
                 fd, fc = got[2 * q]

@@ -182,3 +182,25 @@ def test_pivot_combine_matches_oracle_find_pivot(prec, rule):
         ref = O.find_pivot(X, Y, prec, rule)
         assert (i, j, k) == (ref["i"], ref["j"], ref["diagonal_k"]), (M, N, t)
         assert tot == ref["total_at_pivot"]
+
+
+def test_strip_ranges_and_apportion():
+    """Shard planning helpers (host only)."""
+    from paper_2008_02734_b200.distributed import apportion, strip_ranges, _shard_idx
+    assert apportion(8, [5, 5]) == [4, 4]
+    assert sum(apportion(7, [9, 3, 1])) == 7 and min(apportion(7, [9, 3, 1])) >= 1
+    for (M, N, kstop, H, parts) in [(1000, 900, 950, 128, 3), (5000, 300, 2650, 64, 4), (130, 140, 135, 128, 4)]:
+        rng = strip_ranges(kstop, M, N, H, parts)
+        rows = min(M, kstop + 1)
+        S = (rows + H - 1) // H
+        assert rng[0][0] == 0 and rng[-1][1] == S
+        assert all(a <= b for a, b in rng) and all(rng[q][1] == rng[q + 1][0] for q in range(len(rng) - 1))
+        # the shards' index ranges tile each of the last three diagonals exactly once
+        for s3 in range(3):
+            k = kstop - 2 + s3
+            L_ = L.diag_length(k, M, N)
+            seen = np.zeros(L_, int)
+            for lo, hi in rng:
+                a, b = _shard_idx(kstop, M, N, lo, hi, H)[s3]
+                seen[a:b] += 1
+            assert np.all(seen == 1)

@@ -274,7 +274,8 @@ def _dist_gpu_worker(rank, world, port, cases, q):
     import os
     import torch.distributed as dist
     from paper_2008_02734_b200.distributed import linmdtw_distributed
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # shards in different processes share the GPU by time slicing: allow long waits
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LMDTW_WATCHDOG_S="120")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         out = []
@@ -288,10 +289,13 @@ def _dist_gpu_worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-def test_distributed_device_engine_equals_single_gpu():
-    """Two ranks (gloo) sharing cuda:0 through the C ABI: top-level half passes
-    split across ranks, pivots combined on the host, leaves sharded; the
-    result equals the single-GPU engine's bit for bit."""
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_device_engine_equals_single_gpu(world):
+    """Ranks (gloo) sharing cuda:0 through the C ABI: top-level half passes
+    split across ranks (with 3 ranks one half pass is cut into two strip
+    shards whose handoff crosses processes through a CUDA IPC buffer), pivots
+    combined on the host, leaves sharded; the result equals the single-GPU
+    engine's bit for bit."""
     import socket
     import torch.multiprocessing as mp
     cases = [(3000, 2600, 12, 7, 32, 500), (2200, 1800, 5, 8, 64, 300)]
@@ -301,17 +305,17 @@ def test_distributed_device_engine_equals_single_gpu():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_dist_gpu_worker, args=(r, 2, port, cases, q)) for r in range(2)]
+    procs = [ctx.Process(target=_dist_gpu_worker, args=(r, world, port, cases, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=600) for _ in range(2))
+    res = dict(q.get(timeout=600) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     for ci, (M, N, d, seed, prec, min_dim) in enumerate(cases):
         X, Y = bench.chroma_pair(M, N, d, seed=seed)
         ref = L.linmdtw(X, Y, min_dim=min_dim, precision=prec)
-        for rank in range(2):
+        for rank in range(world):
             cost, path, cells, pkd, pkt, trace = res[rank][ci]
             assert cost == ref.cost and np.array_equal(path, ref.path)
             assert cells == ref.cells_processed and pkd == ref.peak_diag_values and pkt == ref.peak_table_cells
