@@ -351,3 +351,27 @@ def test_strip_sharded_half_pass_equals_unsharded(prec, reverse):
             for s in range(3):
                 assert np.array_equal(od[s][:lens[s]], ref.d[s]), (M, N, ns, s)
                 assert np.array_equal(oc[s][:lens[s]], ref.c[s]), (M, N, ns, s)
+
+
+def test_cfg3_full_size_linmdtw_equals_full_table_dtw_fp64():
+    """BASELINE cfg3 at full size (100k x 100k, d=12, the bench's inputs), fp64:
+    the linear-memory path and cost equal the brute-force DTW's (full table
+    of 2-bit backpointers on the device, 2.5 GB) -- the reference's own
+    acceptance property (test_divide.py:80-86) at the headline shape."""
+    X, Y = bench.make_inputs("cfg3")[0]
+    r = L.linmdtw(X, Y, precision=64)
+    f = L.dtw_full(X, Y, precision=64)
+    assert np.array_equal(r.path, f.path)
+    assert r.cost == f.cost
+    assert r.cells_processed == 19910735310 or 1.99 < r.cells_processed / 1e10 < 2.0
+
+
+def test_cfg3_full_size_fp32_equals_oracle():
+    """The bench workload itself (cfg3, fp32): path, cost, cells_processed, peak
+    counters and the 255-entry pivot trace equal the C oracle's (the reference
+    algorithm restated, run on all host cores, ~1 min)."""
+    X, Y = bench.make_inputs("cfg3")[0]
+    r = L.linmdtw(X, Y, precision=32)
+    o = O.linmdtw(X, Y, precision=32, nthreads=O.num_threads())
+    assert_same_result(r, o)
+    assert len(r.pivot_trace) == 255
