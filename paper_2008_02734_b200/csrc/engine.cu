@@ -361,6 +361,19 @@ struct Engine {
         w.bp = c.bp.as<unsigned long long>();
         w.lb = c.lb.p;
         if (const char* d = getenv("LMDTW_PROBE")) w.dbg = atoi(d);  // LMDTW_PROBES builds only
+        // Latency-bound level: the longest strip has more serial tiles than the
+        // level has tiles per pipeline -> half the pipelines per SM, so the
+        // head strips run with more of their SM (LMDTW_ACTIVE_NP overrides).
+        {
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
+            const int np = pipes_per_cta(prec, dp);
+            int64_t head = 0;
+            for (const auto& p : P) head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
+            const double per_pipe = (double)items.size() / ((double)np * nsm);
+            w.active_np = (head > 2.0 * per_pipe && np >= 2) ? np / 2 : np;
+            if (const char* a = getenv("LMDTW_ACTIVE_NP")) w.active_np = atoi(a);
+        }
         w.flags = c.flags.as<int>();
         w.tab = tab;
         w.leaf_cost = lcost;

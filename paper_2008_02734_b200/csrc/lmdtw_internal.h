@@ -94,11 +94,13 @@ struct WaveLaunch {
     void* lb;               // tile left boundaries (dtype T)
     int* flags;             // tiles completed per strip (zeroed by caller)
     int dbg;                // probe mode (LMDTW_PROBES builds; 0 = normal)
+    int active_np;          // pipelines per CTA taking work (0 = all)
     int grid_warps;         // persistent warps to launch (0 = auto)
     unsigned long long* trace;  // optional per-item timestamps (debug)
 };
 
 int strip_height(int precision, int dp);  // grid rows per strip
+int pipes_per_cta(int precision, int dp);
 int supported_dp(int precision, int d);  // padded dim for d, or -1
 cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
 cudaError_t launch_pivots(int precision, const PassDesc* passes, const PivotDesc* piv, int npiv,
