@@ -15,6 +15,7 @@ for n in (1, 2, 4, 8, 148, 296, 444, 592, 1184):
     ms = C.c_double()
     _capi.check(lib.lmdtw_debug_wave_independent(0, prec, d, n, N, 5, C.byref(ms)))
     cyc = ms.value * 1e-3 * 1.965e9 / (N + 31)
-    cells = n * (128 if prec == 32 else 64) * N
+    H = int(lib.lmdtw_strip_height(prec, d))
+    cells = n * H * N
     print(f"independent strips={n:5d}: {ms.value:8.3f} ms  {cyc:7.1f} cyc/step  {cells / ms.value / 1e6:8.1f} Gcell/s",
           flush=True)
