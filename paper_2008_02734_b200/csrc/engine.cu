@@ -48,6 +48,7 @@ struct Stats {
     long long wave_launches = 0, wave_cells = 0, leaf_cells = 0;
 } g_stats;
 std::atomic<int> g_profile{0};
+cudaEvent_t g_last_sync_ev = nullptr;  // LMDTW_HOST_TIMING diagnostics
 
 int set_err(int code, const std::string& msg) {
     g_err = msg;
@@ -394,6 +395,16 @@ struct Engine {
             fprintf(stderr, "lmdtw host: %zu items prepared in %.1f us\n", items.size(),
                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
         if (prof) CU(cudaEventRecord(c.ev0, c.st));
+        if (getenv("LMDTW_HOST_TIMING")) {  // device-idle gap since the last sync point
+            cudaEvent_t ev;
+            cudaEventCreate(&ev);
+            cudaEventRecord(ev, c.st);
+            cudaEventSynchronize(ev);
+            float ms = 0;
+            if (g_last_sync_ev) cudaEventElapsedTime(&ms, g_last_sync_ev, ev);
+            fprintf(stderr, "lmdtw host: device idle %.1f us before this wave launch\n", 1e3 * ms);
+            cudaEventDestroy(ev);
+        }
         TRY(launched(launch_wave(w, c.st), leaf ? "leaf wave_kernel" : "wave_kernel"));
         if (trace_file) {
             std::vector<unsigned long long> tr(items.size() * 3);
@@ -507,6 +518,10 @@ struct Engine {
         c.d2h += V.size() * sizeof(PivotOut);
         const auto ts0 = std::chrono::steady_clock::now();
         CU(cudaStreamSynchronize(c.st));
+        if (getenv("LMDTW_HOST_TIMING")) {
+            if (!g_last_sync_ev) cudaEventCreate(&g_last_sync_ev);
+            cudaEventRecord(g_last_sync_ev, c.st);
+        }
         if (getenv("LMDTW_HOST_TIMING"))
             fprintf(stderr, "lmdtw host: level waited %.1f us for the device\n",
                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts0).count());
