@@ -121,8 +121,8 @@ struct Ctx {
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     DBuf xraw, yraw, xp, yp, passes, items, counter, out, bnd, pdesc, pout, pscratch, ldesc, bp, path, pcost, plen,
-        lcost, tab, trace, lb, flags;
-    HBuf h_passes, h_items, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
+        lcost, tab, trace, lb, flags, istage;
+    HBuf h_passes, h_items, h_istage, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
     long long call_launches = 0;
     long long h2d = 0, d2h = 0;
 };
@@ -291,31 +291,78 @@ struct Engine {
         const int64_t jend = std::min<int64_t>(p.N - 1, (int64_t)p.kstop - (int64_t)a * H);
         return jend / kTileW + 1;
     }
-    void make_items(const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
-        // key = b*W + a*kLagKey = kLagKey * (b*(W/kLagKey) + a): a counting sort on
-        // m = b*(W/kLagKey) + a, stable in (pass, strip, block) generation order
+    // Host side of the queue build: O(strips + keys) work.  The per-key counts
+    // come from a difference array along each residue class m = a (mod kPer)
+    // (strip a's tiles are the keys a, a+kPer, ..., a+(nb-1)*kPer); their
+    // exclusive prefix sum is each key's first queue slot.  The tiles
+    // themselves are scattered on the device (scatter_items_kernel), so the
+    // host never touches the O(tiles) queue.  Returns the number of tiles.
+    int64_t stage_items(const std::vector<PassDesc>& P, int64_t& nents, int64_t& nkeys) {
         static_assert(kTileW % kLagKey == 0, "tile width must be a multiple of the key lag");
         constexpr int64_t kPer = kTileW / kLagKey;
         int64_t mmax = 0, total = 0;
-        for (const auto& p : P)
+        nents = 0;
+        for (const auto& p : P) {
+            nents += p.strip_hi - p.strip_lo;
             for (int a = p.strip_lo; a < p.strip_hi; a++) {
                 const int64_t nb = tiles_of(p, a, H);
                 mmax = std::max<int64_t>(mmax, (nb - 1) * kPer + a);
                 total += nb;
             }
-        std::vector<int64_t> cnt(mmax + 2, 0);
-        for (const auto& p : P)
-            for (int a = p.strip_lo; a < p.strip_hi; a++) {
-                const int64_t nb = tiles_of(p, a, H);
-                for (int64_t b = 0; b < nb; b++) cnt[b * kPer + a + 1]++;
-            }
-        for (int64_t m = 1; m <= mmax + 1; m++) cnt[m] += cnt[m - 1];
-        items.resize(total);
+        }
+        nkeys = mmax + 1;
+        const size_t ent_bytes = (size_t)nents * sizeof(StripEnt);
+        CU(c.h_istage.ensure(ent_bytes + (size_t)(nkeys + kPer) * sizeof(int32_t)));
+        StripEnt* ents = c.h_istage.as<StripEnt>();
+        int32_t* cnt = reinterpret_cast<int32_t*>(c.h_istage.as<char>() + ent_bytes);
+        std::fill(cnt, cnt + nkeys + kPer, 0);
+        int64_t e = 0;
         for (size_t q = 0; q < P.size(); q++)
             for (int a = P[q].strip_lo; a < P[q].strip_hi; a++) {
                 const int64_t nb = tiles_of(P[q], a, H);
-                for (int64_t b = 0; b < nb; b++) items[cnt[b * kPer + a]++] = WorkItem{(int)q, a, (int)b, 0};
+                ents[e++] = StripEnt{(int32_t)q, a, (int32_t)nb};
+                cnt[a]++;
+                cnt[a + nb * kPer]--;
             }
+        for (int64_t m = kPer; m < nkeys; m++) cnt[m] += cnt[m - kPer];  // per-key tile counts
+        int64_t run = 0;
+        for (int64_t m = 0; m < nkeys; m++) {  // exclusive scan: first slot of key m
+            const int64_t n = cnt[m];
+            cnt[m] = (int32_t)run;
+            run += n;
+        }
+        if (run != total) return -1;
+        return total;
+    }
+
+    // Build the tile queue of passes P in c.items (device), on c.st.
+    int upload_queue(const std::vector<PassDesc>& P, int64_t& nitems) {
+        int64_t nents = 0, nkeys = 0;
+        nitems = stage_items(P, nents, nkeys);
+        if (nitems < 0 || nitems > INT32_MAX) return set_err(LMDTW_EINTERNAL, "tile queue size");
+        const size_t ent_bytes = (size_t)nents * sizeof(StripEnt);
+        const size_t stage_bytes = ent_bytes + (size_t)nkeys * sizeof(int32_t);
+        CU(c.items.ensure((size_t)std::max<int64_t>(nitems, 1) * sizeof(WorkItem)));
+        CU(c.istage.ensure(stage_bytes));
+        CU(cudaMemcpyAsync(c.istage.p, c.h_istage.p, stage_bytes, cudaMemcpyHostToDevice, c.st));
+        return launched(launch_scatter_items(c.istage.as<StripEnt>(), (int)nents,
+                                             reinterpret_cast<int32_t*>(c.istage.as<char>() + ent_bytes),
+                                             (int)(kTileW / kLagKey), c.items.as<WorkItem>(), c.st),
+                        "scatter_items_kernel");
+    }
+
+    // Host-built queue (debug entry points only): same order as the device
+    // scatter up to the order of tiles that share a key.
+    void make_items(const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
+        constexpr int64_t kPer = kTileW / kLagKey;
+        int64_t nents = 0, nkeys = 0;
+        const int64_t total = stage_items(P, nents, nkeys);
+        std::vector<int32_t> cur(c.h_istage.as<int32_t>() + nents * 3, c.h_istage.as<int32_t>() + nents * 3 + nkeys);
+        items.resize(std::max<int64_t>(total, 0));
+        for (size_t q = 0; q < P.size(); q++)
+            for (int a = P[q].strip_lo; a < P[q].strip_hi; a++)
+                for (int64_t b = 0; b < tiles_of(P[q], a, H); b++)
+                    items[cur[b * kPer + a]++] = WorkItem{(int)q, a, (int)b, 0};
     }
 
     int run_wave(const std::vector<PassDesc>& P0, int64_t bnd_total, bool leaf, void* tab, void* lcost,
@@ -334,18 +381,14 @@ struct Engine {
         CU(c.lb.ensure((size_t)std::max<int64_t>(lb_total, 1) * esz));
         CU(c.flags.ensure((size_t)std::max<int64_t>(flag_total, 1) * sizeof(int)));
         CU(cudaMemsetAsync(c.flags.p, 0, (size_t)std::max<int64_t>(flag_total, 1) * sizeof(int), c.st));
-        std::vector<WorkItem> items;
-        make_items(P, items);
         CU(c.h_passes.ensure(P.size() * sizeof(PassDesc)));
-        CU(c.h_items.ensure(items.size() * sizeof(WorkItem)));
         memcpy(c.h_passes.p, P.data(), P.size() * sizeof(PassDesc));
-        memcpy(c.h_items.p, items.data(), items.size() * sizeof(WorkItem));
         CU(c.passes.ensure(P.size() * sizeof(PassDesc)));
-        CU(c.items.ensure(items.size() * sizeof(WorkItem)));
         CU(c.counter.ensure(sizeof(int)));
         CU(c.bnd.ensure((size_t)bnd_total * 8));
         CU(cudaMemcpyAsync(c.passes.p, c.h_passes.p, P.size() * sizeof(PassDesc), cudaMemcpyHostToDevice, c.st));
-        CU(cudaMemcpyAsync(c.items.p, c.h_items.p, items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice, c.st));
+        int64_t nitems = 0;
+        TRY(upload_queue(P, nitems));
         CU(cudaMemsetAsync(c.counter.p, 0, sizeof(int), c.st));
         CU(cudaMemsetAsync(c.bnd.p, 0xFF, (size_t)bnd_total * 8, c.st));  // tag -1
         WaveLaunch w{};
@@ -355,7 +398,7 @@ struct Engine {
         w.precision = prec;
         w.passes = c.passes.as<PassDesc>();
         w.items = c.items.as<WorkItem>();
-        w.nitems = (int)items.size();
+        w.nitems = (int)nitems;
         w.counter = c.counter.as<int>();
         w.out = c.out.p;
         w.bnd = c.bnd.p;
@@ -371,7 +414,7 @@ struct Engine {
             const int np = pipes_per_cta(prec, dp);
             int64_t head = 0;
             for (const auto& p : P) head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
-            const double per_pipe = (double)items.size() / ((double)np * nsm);
+            const double per_pipe = (double)nitems / ((double)np * nsm);
             w.active_np = (head > 2.0 * per_pipe && np >= 2) ? np / 2 : np;
             if (const char* a = getenv("LMDTW_ACTIVE_NP")) w.active_np = atoi(a);
         }
@@ -386,13 +429,13 @@ struct Engine {
         // LMDTW_TRACE_FILE: append per-strip DP start/end timestamps (debug)
         const char* trace_file = getenv("LMDTW_TRACE_FILE");
         if (trace_file) {
-            CU(c.trace.ensure(items.size() * 24));
-            CU(cudaMemsetAsync(c.trace.p, 0, items.size() * 24, c.st));
+            CU(c.trace.ensure(nitems * 24));
+            CU(cudaMemsetAsync(c.trace.p, 0, nitems * 24, c.st));
             w.trace = c.trace.as<unsigned long long>();
         }
         const bool prof = g_profile.load() != 0;
         if (getenv("LMDTW_HOST_TIMING"))
-            fprintf(stderr, "lmdtw host: %zu items prepared in %.1f us\n", items.size(),
+            fprintf(stderr, "lmdtw host: %lld items prepared in %.1f us\n", (long long)nitems,
                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
         if (prof) CU(cudaEventRecord(c.ev0, c.st));
         if (getenv("LMDTW_HOST_TIMING")) {  // device-idle gap since the last sync point
@@ -407,8 +450,10 @@ struct Engine {
         }
         TRY(launched(launch_wave(w, c.st), leaf ? "leaf wave_kernel" : "wave_kernel"));
         if (trace_file) {
-            std::vector<unsigned long long> tr(items.size() * 3);
+            std::vector<unsigned long long> tr(nitems * 3);
+            std::vector<WorkItem> items(nitems);
             CU(cudaMemcpyAsync(tr.data(), c.trace.p, tr.size() * 8, cudaMemcpyDeviceToHost, c.st));
+            CU(cudaMemcpyAsync(items.data(), c.items.p, nitems * sizeof(WorkItem), cudaMemcpyDeviceToHost, c.st));
             CU(cudaStreamSynchronize(c.st));
             if (FILE* f = fopen(trace_file, "ab")) {
                 const long long hdr[3] = {(long long)P.size(), (long long)items.size(), (long long)leaf};
@@ -1015,20 +1060,16 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     pd.flag_off = 0;
     pd.bnd_off = 0;
     pd.bnd_in_first = strip_lo > 0 ? (uint64_t)(uintptr_t)bnd_prev : 0;
-    std::vector<WorkItem> items;
-    E.make_items(std::vector<PassDesc>{pd}, items);
     CU(c->out.ensure((size_t)out_total * E.esz));
     CU(c->passes.ensure(sizeof(PassDesc)));
-    CU(c->items.ensure(items.size() * sizeof(WorkItem)));
     CU(c->counter.ensure(sizeof(int)));
     CU(c->lb.ensure((size_t)pd.nstrips * (H + 1) * E.esz));
     CU(c->flags.ensure((size_t)pd.nstrips * sizeof(int)));
     CU(c->h_passes.ensure(sizeof(PassDesc)));
-    CU(c->h_items.ensure(items.size() * sizeof(WorkItem)));
     memcpy(c->h_passes.p, &pd, sizeof(PassDesc));
-    memcpy(c->h_items.p, items.data(), items.size() * sizeof(WorkItem));
     CU(cudaMemcpyAsync(c->passes.p, c->h_passes.p, sizeof(PassDesc), cudaMemcpyHostToDevice, c->st));
-    CU(cudaMemcpyAsync(c->items.p, c->h_items.p, items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice, c->st));
+    int64_t nitems = 0;
+    TRY(E.upload_queue(std::vector<PassDesc>{pd}, nitems));
     CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
     CU(cudaMemsetAsync(c->flags.p, 0, (size_t)pd.nstrips * sizeof(int), c->st));
     WaveLaunch w{};
@@ -1038,7 +1079,7 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     w.precision = precision;
     w.passes = c->passes.as<PassDesc>();
     w.items = c->items.as<WorkItem>();
-    w.nitems = (int)items.size();
+    w.nitems = (int)nitems;
     w.counter = c->counter.as<int>();
     w.out = c->out.p;
     w.bnd = bnd_local;

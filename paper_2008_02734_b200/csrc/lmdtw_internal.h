@@ -48,6 +48,14 @@ struct WorkItem {
     int32_t pad;
 };
 
+// Queue build input: strip `strip` of pass `pass` has `ntiles` tiles.
+struct StripEnt {
+    int32_t pass;
+    int32_t strip;
+    int32_t ntiles;
+};
+static_assert(sizeof(StripEnt) == 12, "StripEnt is staged as 3 int32");
+
 // Pivot search input: the two passes of one internal node.
 struct PivotDesc {
     int32_t fwd, bwd;       // PassDesc indices
@@ -103,6 +111,10 @@ int strip_height(int precision, int dp);  // grid rows per strip
 int pipes_per_cta(int precision, int dp);
 int supported_dp(int precision, int d);  // padded dim for d, or -1
 cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
+// Tile queue: tile b of entry e goes to slot cursor[b*key_per_tile + strip]++
+// (cursor = first slot of each key, consumed).
+cudaError_t launch_scatter_items(const StripEnt* ents, int nents, int32_t* cursor, int key_per_tile,
+                                 WorkItem* items, cudaStream_t stream);
 cudaError_t launch_pivots(int precision, const PassDesc* passes, const PivotDesc* piv, int npiv,
                           const void* out, PivotOut* res, void* scratch, cudaStream_t stream);
 // scratch for launch_pivots; its per-node counters must start at zero
