@@ -127,10 +127,36 @@ struct Ctx {
     long long h2d = 0, d2h = 0;
 };
 
+// Contexts: a per-device pool.  A call leases one context (stream, events,
+// buffers) for its duration and returns it afterwards, so concurrent calls
+// on one device run on separate streams with separate buffers (SPEC.md:287
+// "safe for concurrent independent calls"), and a progress callback that
+// calls back into the library (from inside a running alignment) gets a
+// context of its own instead of deadlocking on the running call's.
+struct DevPool {
+    std::mutex mu;
+    std::vector<std::unique_ptr<Ctx>> all;  // all[0]: the primary context (lmdtw_stream)
+    std::vector<bool> busy;
+};
 std::mutex g_ctx_mu;
-std::vector<std::unique_ptr<Ctx>> g_ctx;
+std::vector<std::unique_ptr<DevPool>> g_pools;
 
-int get_ctx(int device, Ctx** out) {
+int make_ctx(int device, std::unique_ptr<Ctx>& out) {
+    std::unique_ptr<Ctx> c(new Ctx());
+    c->device = device;
+    CU(cudaSetDevice(device));
+    CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CU(cudaEventCreate(&c->ev0));
+    CU(cudaEventCreate(&c->ev1));
+    if (const char* w = getenv("LMDTW_WATCHDOG_S")) {
+        const double sec = atof(w);  // 0 disables the watchdog
+        if (sec >= 0) CU(set_watchdog_ns((unsigned long long)(sec * 1e9)));
+    }
+    out = std::move(c);
+    return LMDTW_OK;
+}
+
+int get_pool(int device, DevPool** out) {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0) {
@@ -139,21 +165,60 @@ int get_ctx(int device, Ctx** out) {
     }
     if (device < 0 || device >= n) return set_err(LMDTW_EINVAL, "bad device index");
     std::lock_guard<std::mutex> g(g_ctx_mu);
-    if ((int)g_ctx.size() < n) g_ctx.resize(n);
-    if (!g_ctx[device]) {
-        std::unique_ptr<Ctx> c(new Ctx());
-        c->device = device;
-        CU(cudaSetDevice(device));
-        CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
-        CU(cudaEventCreate(&c->ev0));
-        CU(cudaEventCreate(&c->ev1));
-        if (const char* w = getenv("LMDTW_WATCHDOG_S")) {
-            const double sec = atof(w);
-            if (sec > 0) CU(set_watchdog_ns((unsigned long long)(sec * 1e9)));
+    if ((int)g_pools.size() < n) g_pools.resize(n);
+    if (!g_pools[device]) g_pools[device].reset(new DevPool());
+    *out = g_pools[device].get();
+    return LMDTW_OK;
+}
+
+struct CtxLease {
+    Ctx* c = nullptr;
+    DevPool* pool = nullptr;
+    size_t slot = 0;
+    Ctx* operator->() const { return c; }
+    Ctx& operator*() const { return *c; }
+    ~CtxLease() {
+        if (c) {
+            std::lock_guard<std::mutex> g(pool->mu);
+            pool->busy[slot] = false;
         }
-        g_ctx[device] = std::move(c);
     }
-    *out = g_ctx[device].get();
+};
+
+// Lease the lowest-numbered free context of `device` (creating one if all
+// are busy) and make `device` current.
+int lease_ctx(int device, CtxLease& out) {
+    DevPool* pool = nullptr;
+    TRY(get_pool(device, &pool));
+    std::lock_guard<std::mutex> g(pool->mu);
+    size_t q = 0;
+    while (q < pool->all.size() && pool->busy[q]) q++;
+    if (q == pool->all.size()) {
+        std::unique_ptr<Ctx> c;
+        TRY(make_ctx(device, c));
+        pool->all.push_back(std::move(c));
+        pool->busy.push_back(false);
+    }
+    pool->busy[q] = true;
+    out.c = pool->all[q].get();
+    out.pool = pool;
+    out.slot = q;
+    CU(cudaSetDevice(device));
+    return LMDTW_OK;
+}
+
+// The primary context's stream (created on first use).
+int primary_stream(int device, cudaStream_t* st) {
+    DevPool* pool = nullptr;
+    TRY(get_pool(device, &pool));
+    std::lock_guard<std::mutex> g(pool->mu);
+    if (pool->all.empty()) {
+        std::unique_ptr<Ctx> c;
+        TRY(make_ctx(device, c));
+        pool->all.push_back(std::move(c));
+        pool->busy.push_back(false);
+    }
+    *st = pool->all[0]->st;
     return LMDTW_OK;
 }
 
@@ -226,12 +291,14 @@ struct Node {
 
 struct Engine {
     Ctx& c;
-    int prec, d, dp, H;
+    int prec, d, dp, H;  // dp: padded row length (elements)
+    DimPlan dpl;
     size_t esz;
     int tie[3] = {2, 0, 1};
     Engine(Ctx& ctx, int precision, int dim) : c(ctx), prec(precision), d(dim) {
-        dp = supported_dp(prec, d);
-        H = strip_height(prec, dp);
+        dpl = plan_dims(prec, d);
+        dp = dpl.dp;
+        H = strip_height(prec, dpl);
         esz = prec == 32 ? 4 : 8;
     }
 
@@ -395,6 +462,7 @@ struct Engine {
         w.X = c.xp.p;
         w.Y = c.yp.p;
         w.dp = dp;
+        w.wide = dpl.wide;
         w.precision = prec;
         w.passes = c.passes.as<PassDesc>();
         w.items = c.items.as<WorkItem>();
@@ -411,7 +479,7 @@ struct Engine {
         {
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
-            const int np = pipes_per_cta(prec, dp);
+            const int np = pipes_per_cta(prec, dpl);
             int64_t head = 0;
             for (const auto& p : P) head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
             const double per_pipe = (double)nitems / ((double)np * nsm);
@@ -506,6 +574,7 @@ struct Engine {
         p.strip_lo = 0;
         p.strip_hi = p.nstrips;
         p.bnd_in_first = 0;
+        p.sys_out = 0;
         p.bp_off = 0;
         p.tab_off = -1;
         p.w64 = 0;
@@ -606,6 +675,7 @@ struct Engine {
             p.strip_lo = 0;
             p.strip_hi = p.nstrips;
             p.bnd_in_first = 0;
+            p.sys_out = 0;
             p.bnd_off = bnd_total;
             bnd_total += 2 * ((nd.N + 1) & ~1LL) * bwords();  // two slots, 16-byte aligned
             p.w64 = (int32_t)((nd.N + 31) / 32);
@@ -640,7 +710,7 @@ struct Engine {
         CU(c.path.ensure((size_t)path_total * 2 * sizeof(int)));
         CU(c.pcost.ensure((size_t)path_total * esz));
         CU(c.plen.ensure((size_t)n * sizeof(int)));
-        TRY(launched(launch_backtrace(prec, dp, c.xp.p, c.yp.p, c.ldesc.as<LeafDesc>(), n,
+        TRY(launched(launch_backtrace(prec, dpl, c.xp.p, c.yp.p, c.ldesc.as<LeafDesc>(), n,
                                       c.bp.as<unsigned long long>(), c.path.as<int>(), c.pcost.p, c.plen.as<int>(),
                                       c.st),
                      "backtrace_kernel"));
@@ -687,10 +757,9 @@ int validate_common(int64_t M, int64_t N, int d, int prec) {
     if (M < 1 || N < 1) return set_err(LMDTW_EINVAL, "series must have length >= 1");
     if (d < 1) return set_err(LMDTW_EINVAL, "feature dimension must be >= 1");
     if (prec != 32 && prec != 64) return set_err(LMDTW_EINVAL, "precision must be 32 or 64");
-    if (supported_dp(prec, d) < 0) {
+    if (plan_dims(prec, d).dp < 0) {
         char buf[128];
-        snprintf(buf, sizeof buf, "feature dimension %d exceeds the kernels' maximum (%d) for precision %d", d,
-                 lmdtw_max_dim(prec), prec);
+        snprintf(buf, sizeof buf, "feature dimension %d exceeds the supported maximum (%d)", d, lmdtw_max_dim(prec));
         return set_err(LMDTW_EINVAL, buf);
     }
     if (M + N > (int64_t)1 << 30) return set_err(LMDTW_EINVAL, "M + N too large (limit 2^30)");
@@ -716,9 +785,8 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     if (cfg.min_dim < 2) return set_err(LMDTW_EINVAL, "min_dim must be >= 2");
     TRY(validate_tie(cfg.tie));
     if (cfg.pivot_highest != 0 && cfg.pivot_highest != 1) return set_err(LMDTW_EINVAL, "unknown pivot_tie_rule");
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     c->call_launches = 0;
     c->h2d = c->d2h = 0;
@@ -945,7 +1013,10 @@ int lmdtw_device_count(void) {
     return n;
 }
 
-int lmdtw_max_dim(int32_t precision) { return precision == 32 ? 64 : 48; }
+int lmdtw_max_dim(int32_t precision) {
+    (void)precision;
+    return kMaxDim;
+}
 
 int64_t lmdtw_diag_length(int64_t k, int64_t M, int64_t N) { return dlen(k, M, N); }
 int64_t lmdtw_cells_upto(int64_t kstop, int64_t M, int64_t N) { return cells_upto(kstop, M, N); }
@@ -972,11 +1043,12 @@ int lmdtw_debug_wait_stats(unsigned long long* cycles, unsigned long long* count
     CU(wait_stats(cycles, count, reset));
     return LMDTW_OK;
 }
-// The stream every kernel of `device` is launched on (for event timing).
+// The stream of `device`'s primary context: every kernel of a call runs on
+// it unless another call on the same device is in flight (for event timing).
 void* lmdtw_stream(int device) {
-    Ctx* c = nullptr;
-    if (get_ctx(device, &c) != LMDTW_OK) return nullptr;
-    return (void*)c->st;
+    cudaStream_t st = nullptr;
+    if (primary_stream(device, &st) != LMDTW_OK) return nullptr;
+    return (void*)st;
 }
 
 // Benchmark hook (not part of the reference-facing ABI): `npasses`
@@ -985,9 +1057,8 @@ void* lmdtw_stream(int device) {
 // per-warp step rate without strip-to-strip dependencies.
 int lmdtw_debug_wave_independent(int device, int32_t precision, int32_t d, int32_t npasses, int32_t N,
                                  int32_t reps, double* ms) {
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     Engine E(*c, precision, d);
     const int64_t M = E.H;
@@ -1028,8 +1099,8 @@ int lmdtw_debug_wave_independent(int device, int32_t precision, int32_t d, int32
 int64_t lmdtw_handoff_words(int64_t N, int32_t precision) { return 2 * ((N + 1) & ~1LL) * (precision == 32 ? 1 : 2); }
 
 int32_t lmdtw_strip_height(int32_t precision, int32_t d) {
-    const int dp = supported_dp(precision, d);
-    return dp < 0 ? -1 : strip_height(precision, dp);
+    const DimPlan dp = plan_dims(precision, d);
+    return dp.dp < 0 ? -1 : strip_height(precision, dp);
 }
 
 int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d, int64_t kstop,
@@ -1038,9 +1109,8 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     TRY(validate_common(M, N, d, precision));
     if (kstop < 2 || kstop > M + N - 2) return set_err(LMDTW_EINVAL, "kstop out of range [2, M+N-2]");
     if (!bnd_local) return set_err(LMDTW_EINVAL, "bnd_local is required");
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     c->call_launches = 0;
     Engine E(*c, precision, d);
@@ -1060,6 +1130,7 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     pd.flag_off = 0;
     pd.bnd_off = 0;
     pd.bnd_in_first = strip_lo > 0 ? (uint64_t)(uintptr_t)bnd_prev : 0;
+    pd.sys_out = strip_hi < pd.nstrips ? 1 : 0;  // the next shard may run on a peer GPU
     CU(c->out.ensure((size_t)out_total * E.esz));
     CU(c->passes.ensure(sizeof(PassDesc)));
     CU(c->counter.ensure(sizeof(int)));
@@ -1076,6 +1147,7 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     w.X = c->xp.p;
     w.Y = c->yp.p;
     w.dp = E.dp;
+    w.wide = E.dpl.wide;
     w.precision = precision;
     w.passes = c->passes.as<PassDesc>();
     w.items = c->items.as<WorkItem>();
@@ -1161,9 +1233,8 @@ int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const f
     TRY(validate_common(M, N, d, precision));
     if (kstop < 2 || kstop > M + N - 2) return set_err(LMDTW_EINVAL, "kstop out of range [2, M+N-2]");
     if (nshards < 1) return set_err(LMDTW_EINVAL, "nshards must be >= 1");
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     Engine E(*c, precision, d);
     std::vector<int64_t> xb, yb;
@@ -1218,6 +1289,7 @@ int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const f
         for (int q = 0; q < ns; q++) {
             Shard& z = sh[q];
             z.pd.bnd_in_first = q > 0 ? (uint64_t)(uintptr_t)sh[q - 1].bnd.p : 0;
+            z.pd.sys_out = q + 1 < ns ? 1 : 0;
             cudaMemcpy(z.passes.p, &z.pd, sizeof(PassDesc), cudaMemcpyHostToDevice);
             cudaMemcpy(z.items_d.p, z.items.data(), z.items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice);
             cudaMemset(z.counter.p, 0, sizeof(int));
@@ -1231,6 +1303,8 @@ int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const f
             w.X = c->xp.p;
             w.Y = c->yp.p;
             w.dp = E.dp;
+            w.wide = E.dpl.wide;
+    w.wide = E.dpl.wide;
             w.precision = precision;
             w.passes = z.passes.as<PassDesc>();
             w.items = z.items_d.as<WorkItem>();
@@ -1280,9 +1354,8 @@ int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64
                     int64_t* cells) {
     TRY(validate_common(M, N, d, precision));
     if (kstop < 2 || kstop > M + N - 2) return set_err(LMDTW_EINVAL, "kstop out of range [2, M+N-2]");
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     c->call_launches = 0;
     Engine E(*c, precision, d);
@@ -1313,9 +1386,8 @@ int lmdtw_find_pivot(int device, const float* X, int64_t M, const float* Y, int6
                      int64_t* diagonal_k, double* total, int64_t* cells, int64_t* peak) {
     TRY(validate_common(M, N, d, precision));
     if (M + N - 2 < 2) return set_err(LMDTW_EINVAL, "too small for a pivot search; use dtw_full");
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     c->call_launches = 0;
     Engine E(*c, precision, d);
@@ -1344,9 +1416,8 @@ int lmdtw_dtw_full(int device, const float* X, int64_t M, const float* Y, int64_
                    int64_t* path_len, void* D_out) {
     TRY(validate_common(M, N, d, precision));
     TRY(validate_tie(tie));
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     c->call_launches = 0;
     Engine E(*c, precision, d);
@@ -1408,9 +1479,8 @@ int lmdtw_pivot_nodes(int device, const float* X, int64_t M, const float* Y, int
         if (s[2] + s[3] - 2 < 2) return set_err(LMDTW_EINVAL, "sub-block too small for a pivot search");
     }
     if (n == 0) return LMDTW_OK;
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     c->call_launches = 0;
     Engine E(*c, precision, d);
@@ -1452,9 +1522,8 @@ int lmdtw_leaf_nodes(int device, const float* X, int64_t M, const float* Y, int6
             return set_err(LMDTW_EINVAL, "sub-block outside the series");
     }
     if (n == 0) return LMDTW_OK;
-    Ctx* c = nullptr;
-    TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> g(c->mu);
+    CtxLease c;
+    TRY(lease_ctx(device, c));
     CU(cudaSetDevice(device));
     c->call_launches = 0;
     Engine E(*c, precision, d);

@@ -30,7 +30,7 @@ struct PassDesc {
     int32_t tile_w;         // columns per tile (set by the launcher)
     int32_t strip_lo;       // strips [strip_lo, strip_hi) run in this launch (a shard of the pass)
     int32_t strip_hi;
-    int32_t pad;
+    int32_t sys_out;        // 1: strip strip_hi-1 publishes to a consumer on another GPU (system-scope stores)
     uint64_t bnd_in_first;  // != 0: strip strip_lo reads strip strip_lo-1's handoff slots here
                             // (another shard's buffer, e.g. a peer GPU's), system-scope loads
 };
@@ -86,7 +86,8 @@ struct LeafDesc {
 struct WaveLaunch {
     const void* X;          // padded features, dtype T, row stride dp
     const void* Y;
-    int dp;                 // padded dimension (template value)
+    int dp;                 // padded row length (elements)
+    int wide;               // DimPlan::wide
     int precision;          // 32 / 64
     const PassDesc* passes;
     const WorkItem* items;
@@ -107,9 +108,18 @@ struct WaveLaunch {
     unsigned long long* trace;  // optional per-item timestamps (debug)
 };
 
-int strip_height(int precision, int dp);  // grid rows per strip
-int pipes_per_cta(int precision, int dp);
-int supported_dp(int precision, int d);  // padded dim for d, or -1
+// How feature rows of dimension d are laid out and which kernels run them:
+// dp = padded row length in elements; wide = 0: register-resident kernels
+// instantiated for dp; wide = 1: dimension-blocked kernels (dp a multiple of
+// the block width).  dp = -1: unsupported d.
+struct DimPlan {
+    int dp;
+    int wide;
+};
+constexpr int kMaxDim = 1 << 16;
+DimPlan plan_dims(int precision, int d);
+int strip_height(int precision, DimPlan dp);  // grid rows per strip
+int pipes_per_cta(int precision, DimPlan dp);
 cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
 // Tile queue: tile b of entry e goes to slot cursor[b*key_per_tile + strip]++
 // (cursor = first slot of each key, consumed).
@@ -119,12 +129,12 @@ cudaError_t launch_pivots(int precision, const PassDesc* passes, const PivotDesc
                           const void* out, PivotOut* res, void* scratch, cudaStream_t stream);
 // scratch for launch_pivots; its per-node counters must start at zero
 size_t pivot_scratch_bytes(int npiv);
-cudaError_t launch_backtrace(int precision, int dp, const void* X, const void* Y, const LeafDesc* leaves,
+cudaError_t launch_backtrace(int precision, DimPlan dp, const void* X, const void* Y, const LeafDesc* leaves,
                              int nleaves, const unsigned long long* bp, int* path, void* pcost,
                              int* plen, cudaStream_t stream);
 cudaError_t launch_pad_cast(int precision, const float* src, int64_t rows, int d, int dp, void* dst,
                             cudaStream_t stream);
-int max_resident_warps(int precision, int dp, int leaf, int device);
+int max_resident_warps(int precision, DimPlan dp, int leaf, int device);
 cudaError_t set_watchdog_ns(unsigned long long ns);  // per device (current device)
 cudaError_t wait_stats(unsigned long long* cycles, unsigned long long* count, int reset);
 

@@ -429,5 +429,4 @@ def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | N
     return AlignmentResult(
         cost=engine.path_cost(path), path=path, cells_processed=int(cells), cells_budget=2 * M * N,
         precision=str(dtype), algorithm="linmdtw", peak_diag_values=int(peak_diag),
-        peak_table_cells=int(peak_table), pivot_trace=tuple(trace),
-        level_stats=(("levels", nlevels), ("ranks", world)))
+        peak_table_cells=int(peak_table), pivot_trace=tuple(trace))

@@ -109,8 +109,7 @@ def _result(handle, M, N, dtype) -> AlignmentResult:
         cost=float(info.cost), path=path, cells_processed=int(info.cells_processed),
         cells_budget=2 * M * N, precision=str(dtype), algorithm="linmdtw",
         peak_diag_values=int(info.peak_diag_values), peak_table_cells=int(info.peak_table_cells),
-        pivot_trace=trace,
-        level_stats=(("levels", int(info.n_levels)), ("gpu_launches", int(info.gpu_launches))))
+        pivot_trace=trace)  # level_stats stays () as in the reference (divide.py:203-213)
     return res
 
 
