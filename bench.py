@@ -13,10 +13,11 @@ value  : inputs resident in HBM (device pointers through the C ABI), CUDA
 e2e    : the public drop-in call linmdtw(FeatureSeries, ...) on pinned host
          buffers: H2D copies, all kernels, path D2H and host stitching timed.
 roofline: the strip-wavefront kernel's cell updates/s (CUDA events around
-         every half-pass launch in the timed steps) against the FP32 cell-
+         every half-pass launch in the timed steps, read back at the engine's
+         own sync points, so timing adds no host sync) against the FP32 cell-
          update roofline of SURVEY.md 8(d): N_SM * 128 * f_max / (2d + 5).
-cpu_baseline: the C oracle (oracle/, a restatement of the reference) on a
-         bounded sample, single-threaded.
+cpu_baseline: the C oracle (oracle/, a restatement of the reference) with
+         all host threads on the same workload (cfg4: a stated subsample).
 """
 from __future__ import annotations
 
@@ -204,16 +205,62 @@ def fp32_cell_roofline(d, n_sm, f_mhz):
     return n_sm * 128 * f_mhz * 1e6 / (2 * d + 5)
 
 
-def cpu_sample(prec=32, nthreads=1, M=20000, N=20000, seed=3):
-    """Oracle linmdtw on a bounded sample of the workload: a cfg3-generator pair
-    at 20k x 20k (cfg2 shape).  Returns (gcups, seconds, cells)."""
+# cfg4 on the CPU: a stated subsample of the batch (the whole batch is ~1.6e11 cells)
+CPU_CFG4_PAIRS = 8
+
+
+def cpu_workload(name, min_dim=500):
+    """The CPU leg's sample of config `name`: the whole workload (the same
+    inputs the GPU arm aligns) except cfg4, where the first CPU_CFG4_PAIRS
+    pairs of the batch are aligned.  Returns (pairs, description)."""
+    pairs = make_inputs(name)
+    c = CONFIGS[name]
+    if name == "cfg4":
+        pairs = pairs[:CPU_CFG4_PAIRS]
+        return pairs, f"first {len(pairs)} of the 256 cfg4 pairs (same inputs as the GPU arm)"
+    return pairs, f"the whole {name} workload: {c['workload']} (same inputs as the GPU arm)"
+
+
+def cpu_run(name, pairs, nthreads, min_dim=500):
+    """The oracle (C restatement of the reference, test infrastructure) over
+    `pairs` with `nthreads` host threads.  Returns (gcups, seconds, cells)."""
     from oracle import oracle as O
     O.build()
-    X, Y = chroma_pair(M, N, 12, seed=seed)
+    prec = CONFIGS[name]["prec"]
+    cells = 0
     t = time.perf_counter()
-    r = O.linmdtw(X, Y, min_dim=500, precision=prec, nthreads=nthreads)
+    for X, Y in pairs:
+        cells += O.linmdtw(X, Y, min_dim=min_dim, precision=prec, nthreads=nthreads)["cells_processed"]
     dt = time.perf_counter() - t
-    return r["cells_processed"] / dt / 1e9, dt, r["cells_processed"]
+    return cells / dt / 1e9, dt, cells
+
+
+def numba_reference_cfg2():
+    """The real reference (Python + numba, installed unmodified in
+    baseline/_ref) on cfg2 in fp32, one core (numba holds the GIL), JIT warmed
+    on cfg1 first.  None when it cannot be imported on this host."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "lmdtw")):
+        return None
+    code = (
+        "import sys, time, json\n"
+        f"sys.path.insert(0, {ref!r}); sys.path.insert(1, {ROOT!r})\n"
+        "import lmdtw, bench\n"
+        "X, Y = bench.make_inputs('cfg1')[0]\n"
+        "lmdtw.linmdtw(X, Y, precision=32)\n"
+        "X, Y = bench.make_inputs('cfg2')[0]\n"
+        "t = time.perf_counter(); r = lmdtw.linmdtw(X, Y, precision=32); dt = time.perf_counter() - t\n"
+        "print(json.dumps({'cells': int(r.cells_processed), 'secs': dt, 'cost': float(r.cost)}))\n")
+    env = dict(os.environ, NUMBA_CACHE_DIR="/tmp/lmdtw_numba_cache", PYTHONDONTWRITEBYTECODE="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240,
+                             env=env, cwd="/tmp")
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+    return {"value": round(r["cells"] / r["secs"] / 1e9, 4), "unit": "GCUPS", "cores": 1, "kind": "reference",
+            "seconds": round(r["secs"], 2), "cost": r["cost"],
+            "sample": "unmodified reference lmdtw.linmdtw (baseline/_ref, numba) on cfg2 20000x20000 d=12 fp32"}
 
 
 def cpu_desc():
@@ -242,36 +289,45 @@ def _allreduce(v: float, op: str) -> float:
 
 # ------------------------------------------------------------------ arms
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (the C oracle restating
-    it; the reference itself is Python+numba and is not shipped to the box)
-    with all host threads, one bounded sample per step."""
+    """--impl reference: the reference's CPU algorithm on this host -- the C
+    oracle restating it (the reference itself is Python + numba and holds
+    the GIL, so it is effectively one core) with all host threads, on the same
+    config, inputs and metric as our arm.  Each timed step is the whole
+    workload (cfg4: a stated subsample); the warm-up steps run cfg1 (there is
+    no JIT to warm).  The real numba reference is timed on cfg2 beside it."""
     if rank != 0:
         return
     from oracle import oracle as O
     O.build()
     nthreads = O.num_threads()
-    X, Y = chroma_pair(20000, 20000, 12, seed=3)
-    vals = []
-    for s in range(args.warmup + args.steps):
-        t = time.perf_counter()
-        r = O.linmdtw(X, Y, min_dim=500, precision=32, nthreads=nthreads)
-        dt = time.perf_counter() - t
-        if s >= args.warmup:
-            vals.append((r["cells_processed"], dt))
-    cells = sum(c for c, _ in vals)
-    secs = sum(t for _, t in vals)
+    pairs, desc = cpu_workload(args.config, args.min_dim)
+    warm = make_inputs("cfg1")
+    for _ in range(args.warmup):
+        cpu_run("cfg1", warm, nthreads)
+    cells, secs = 0, 0.0
+    for _ in range(args.steps):
+        _, dt, c = cpu_run(args.config, pairs, nthreads, args.min_dim)
+        cells += c
+        secs += dt
     gcups = cells / secs / 1e9
     model, ncpu = cpu_desc()
+    prec = CONFIGS[args.config]["prec"]
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gcups, 4), "unit": "GCUPS",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * secs / len(vals), 2), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "chroma-like 20000x20000 d=12 seed 3 (bounded sample of cfg3), min_dim=500"},
+        "ms_per_step": round(1e3 * secs / args.steps, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config]["workload"], "min_dim": args.min_dim, "precision": prec,
+                   "cells_per_step": cells // args.steps, "same_config": args.config != "cfg4",
+                   "sample": desc},
         "cpu_baseline": {"value": round(gcups, 4), "unit": "GCUPS", "cores": nthreads, "kind": "port",
-                         "sample": f"oracle linmdtw 20000x20000 fp32 per step; {model}, nproc={ncpu}"},
+                         "sample": f"oracle linmdtw (C restatement of the reference), {desc}, per step; "
+                                   f"{model}, nproc={ncpu}"},
         "e2e": {"value": round(gcups, 4), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_cpu:
+        nb = numba_reference_cfg2()
+        line["reference_numba"] = nb if nb is not None else {"unavailable": "numba reference not importable"}
     print(json.dumps(line), flush=True)
 
 
@@ -405,6 +461,25 @@ def run_ours(args, rank, world):
         if not dist_single:
             ecells = int(_allreduce(float(ecells), "sum"))
     e2e_value = (ecells / len(ems)) / (e2e_ms / 1e3) / 1e9
+    # the reference's natural inputs: pageable numpy arrays (FeatureSeries)
+    page = [(L.FeatureSeries(X), L.FeatureSeries(Y)) for X, Y in pairs]
+
+    def one_pageable():
+        if dist_single:
+            return linmdtw_distributed(page[0][0], page[0][1], config=cfg).cells_processed, None
+        if len(page) == 0:
+            return 0, None
+        if len(page) == 1:
+            return L.linmdtw(page[0][0], page[0][1], config=cfg).cells_processed, None
+        return sum(r.cells_processed for r in L.align_batch(page, config=cfg)), None
+
+    pms, pcells, _ = timed(one_pageable, max(1, min(args.steps, 3)))
+    page_ms = sum(pms) / len(pms)
+    if world > 1:
+        page_ms = _allreduce(page_ms, "max")
+        if not dist_single:
+            pcells = int(_allreduce(float(pcells), "sum"))
+    page_value = (pcells / len(pms)) / (page_ms / 1e3) / 1e9
     h2d = sum(X.nbytes + Y.nbytes for X, Y in pairs)
     K = sum(X.shape[0] + Y.shape[0] for X, Y in pairs)
     d2h = K * 16  # path (i,j) int64 pairs ~ M+N per alignment (upper bound)
@@ -441,6 +516,8 @@ def run_ours(args, rank, world):
         "e2e": {"value": round(e2e_value, 3), "unit": "GCUPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
                 "api": "paper_2008_02734_b200.linmdtw (pinned host FeatureSeries)"},
+        "e2e_pageable": {"value": round(page_value, 3), "unit": "GCUPS", "ms_per_step": round(page_ms, 3),
+                         "api": "paper_2008_02734_b200.linmdtw (pageable numpy FeatureSeries)"},
         "roofline": {"bound": "fp32", "kernel": "wave_kernel (half passes)", "achieved": round(wave_rate / 1e9, 2),
                      "peak": round(roof / 1e9, 2), "unit": "Gcell/s", "frac": round(wave_rate / roof, 4),
                      "traffic": traffic, "traffic_basis": traffic_basis,
@@ -450,11 +527,14 @@ def run_ours(args, rank, world):
         "gpu_launches": launches,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        g, secs, ncell = cpu_sample(prec=32, nthreads=1)
+        from oracle import oracle as O
+        nthreads = O.num_threads()
+        cpairs, desc = cpu_workload(args.config, args.min_dim)
+        g, secs, ncell = cpu_run(args.config, cpairs, nthreads, args.min_dim)
         model, ncpu = cpu_desc()
-        line["cpu_baseline"] = {"value": round(g, 4), "unit": "GCUPS", "cores": 1, "kind": "port",
-                                "sample": f"oracle linmdtw chroma 20000x20000 d=12 fp32 ({ncell} cells, "
-                                          f"{secs:.1f} s); {model}, nproc={ncpu}"}
+        line["cpu_baseline"] = {"value": round(g, 4), "unit": "GCUPS", "cores": nthreads, "kind": "port",
+                                "sample": f"oracle linmdtw (C restatement of the reference), {desc}: "
+                                          f"{ncell} cells in {secs:.1f} s; {model}, nproc={ncpu}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -117,6 +117,10 @@ int64_t orc_half_pass_##SFX(const float *X, int64_t xstride, const float *Y,    
         T *D2 = bufD[k % 3], *C2 = bufC[k % 3];                                           \
         const T *Dm1 = bufD[(k + 2) % 3], *Dm2 = bufD[(k + 1) % 3];                       \
         int64_t i0 = LMIN(k, M - 1), i0m1 = LMIN(k - 1, M - 1), i0m2 = LMIN(k - 2, M - 1); \
+        /* cells of one diagonal are independent: long diagonals are split    */         \
+        /* into tasks (inside the linmdtw parallel region); results never     */         \
+        /* depend on the thread count                                         */         \
+        _Pragma("omp taskloop grainsize(4096) if(L >= 16384)")                            \
         for (int64_t idx = 0; idx < L; idx++) {                                           \
             int64_t i = i0 - idx, j = k - i;                                              \
             T c = cost_##SFX(X + i * xstride, Y + j * ystride, d);                         \

@@ -125,7 +125,54 @@ struct Ctx {
     HBuf h_passes, h_items, h_istage, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
     long long call_launches = 0;
     long long h2d = 0, d2h = 0;
+    // profiling (lmdtw_profile_enable): events around wave launches, read
+    // back at the next stream sync, so timing never adds a host sync
+    struct Pend {
+        int e0, e1;
+        long long cells;
+        bool leaf;
+    };
+    std::vector<cudaEvent_t> evpool;
+    std::vector<Pend> pend;
+    int ev_used = 0;
+    cudaError_t prof_event(int* idx) {
+        if (ev_used == (int)evpool.size()) {
+            cudaEvent_t e;
+            cudaError_t r = cudaEventCreate(&e);
+            if (r != cudaSuccess) return r;
+            evpool.push_back(e);
+        }
+        *idx = ev_used++;
+        return cudaSuccess;
+    }
+    // call after a stream sync: every pending event has completed
+    void prof_collect();
 };
+
+void Ctx::prof_collect() {
+    if (pend.empty()) {
+        ev_used = 0;
+        return;
+    }
+    std::lock_guard<std::mutex> g(g_stats.mu);
+    for (const Pend& p : pend) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, evpool[p.e0], evpool[p.e1]) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (p.leaf) {
+            g_stats.leaf_ms += ms;
+            g_stats.leaf_cells += p.cells;
+        } else {
+            g_stats.wave_ms += ms;
+            g_stats.wave_launches += 1;
+            g_stats.wave_cells += p.cells;
+        }
+    }
+    pend.clear();
+    ev_used = 0;
+}
 
 // Contexts: a per-device pool.  A call leases one context (stream, events,
 // buffers) for its duration and returns it afterwards, so concurrent calls
@@ -505,7 +552,12 @@ struct Engine {
         if (getenv("LMDTW_HOST_TIMING"))
             fprintf(stderr, "lmdtw host: %lld items prepared in %.1f us\n", (long long)nitems,
                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
-        if (prof) CU(cudaEventRecord(c.ev0, c.st));
+        int pe0 = -1, pe1 = -1;
+        if (prof) {
+            CU(c.prof_event(&pe0));
+            CU(c.prof_event(&pe1));
+            CU(cudaEventRecord(c.evpool[pe0], c.st));
+        }
         if (getenv("LMDTW_HOST_TIMING")) {  // device-idle gap since the last sync point
             cudaEvent_t ev;
             cudaEventCreate(&ev);
@@ -533,19 +585,8 @@ struct Engine {
             }
         }
         if (prof) {
-            CU(cudaEventRecord(c.ev1, c.st));
-            CU(cudaEventSynchronize(c.ev1));
-            float ms = 0;
-            CU(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
-            std::lock_guard<std::mutex> g(g_stats.mu);
-            if (leaf) {
-                g_stats.leaf_ms += ms;
-                g_stats.leaf_cells += cells;
-            } else {
-                g_stats.wave_ms += ms;
-                g_stats.wave_launches += 1;
-                g_stats.wave_cells += cells;
-            }
+            CU(cudaEventRecord(c.evpool[pe1], c.st));
+            c.pend.push_back(Ctx::Pend{pe0, pe1, (long long)cells, leaf});
         }
         return LMDTW_OK;
     }
@@ -632,6 +673,7 @@ struct Engine {
         c.d2h += V.size() * sizeof(PivotOut);
         const auto ts0 = std::chrono::steady_clock::now();
         CU(cudaStreamSynchronize(c.st));
+        c.prof_collect();
         if (getenv("LMDTW_HOST_TIMING")) {
             if (!g_last_sync_ev) cudaEventCreate(&g_last_sync_ev);
             cudaEventRecord(g_last_sync_ev, c.st);
@@ -729,6 +771,7 @@ struct Engine {
             c.d2h += tb;
         }
         CU(cudaStreamSynchronize(c.st));
+        c.prof_collect();
         plen.assign(c.h_plen.as<int>(), c.h_plen.as<int>() + n);
         for (int q = 0; q < n; q++)
             if (plen[q] < 0) {
@@ -1178,6 +1221,7 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
                                cnt * E.esz, cudaMemcpyDeviceToHost, c->st));
     }
     CU(cudaStreamSynchronize(c->st));
+    c->prof_collect();
     if (cells) {
         const int64_t ra = (int64_t)strip_lo * H, rb = std::min<int64_t>(pd.rows, (int64_t)strip_hi * H);
         *cells = cells_upto(kstop, rb, N) - cells_upto(kstop, ra, N);
@@ -1241,6 +1285,7 @@ int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const f
     TRY(E.stage(&X, &M, 1, LMDTW_MEM_HOST, true, xb));
     TRY(E.stage(&Y, &N, 1, LMDTW_MEM_HOST, false, yb));
     CU(cudaStreamSynchronize(c->st));
+    c->prof_collect();
     int64_t out_total = 0, bnd_total = 0;
     const PassDesc base = E.half_pass_desc(xb[0], yb[0], M, N, kstop, reverse ? 1 : 0, out_total, bnd_total);
     const int S = base.nstrips, H = E.H;
@@ -1377,6 +1422,7 @@ int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64
                                cudaMemcpyDeviceToHost, c->st));
     }
     CU(cudaStreamSynchronize(c->st));
+    c->prof_collect();
     if (cells) *cells = cl;
     return LMDTW_OK;
 }

@@ -30,3 +30,34 @@ def trace_from(case):
         e["total_at_pivot"] = float(tot)
         out.append(e)
     return out
+
+
+def acceptance_c1():
+    """Criterion-1 sweep records (tests/golden/make_acceptance.py): per instance
+    the inputs (regenerated from the seeds as the reference's random_series
+    does), the certified minimum cost, and the reference's linmdtw result
+    (cost, path, pivot trace) in fp32 and fp64."""
+    with np.load(os.path.join(GOLDEN, "acceptance_c1.npz")) as f:
+        z = {k: f[k] for k in f.files}  # npz members decompress on every access
+    keys = ("i", "j", "i_off", "j_off", "M", "N", "sub_i", "sub_j", "diagonal_k")
+    out = []
+    po = {32: 0, 64: 0}
+    vo = {32: 0, 64: 0}
+    for q, (dim, M, N, rep, seed) in enumerate(z["meta"]):
+        X = np.random.default_rng(int(seed)).standard_normal((int(M), int(dim))).astype(np.float32)
+        Y = np.random.default_rng(int(seed) + 7).standard_normal((int(N), int(dim))).astype(np.float32)
+        rec = {"X": X, "Y": Y, "dag_cost": float(z["dag_cost"][q])}
+        for prec in (32, 64):
+            n = int(z[f"plen{prec}"][q])
+            path = z[f"path{prec}"][po[prec]:po[prec] + n].astype(np.int64)
+            po[prec] += n
+            k = int(z[f"npiv{prec}"][q])
+            trace = []
+            for row, tot in zip(z[f"piv{prec}"][vo[prec]:vo[prec] + k], z[f"ptot{prec}"][vo[prec]:vo[prec] + k]):
+                e = {kk: int(v) for kk, v in zip(keys, row)}
+                e["total_at_pivot"] = float(tot)
+                trace.append(e)
+            vo[prec] += k
+            rec[prec] = {"cost": float(z[f"cost{prec}"][q]), "path": path, "trace": trace}
+        out.append(rec)
+    return out

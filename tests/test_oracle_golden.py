@@ -61,3 +61,18 @@ def test_cfg1_golden_values():
     assert float(c64["cost"]) == 11.1431643162049
     assert float(c32["cost"]) == 11.14316463470459
     assert int(c64["cells"]) == 1501687 and len(c64["path"]) == 1073
+
+
+def test_acceptance_c1_sweep_oracle():
+    """Reference acceptance criterion 1 (test_acceptance.py:40-74): 2,178 tiny
+    instances at min_dim=2.  The oracle's linmdtw equals the reference's result
+    (cost, path, pivot trace) in fp64 and fp32, and the fp64 cost equals the
+    OptimalPathDag-certified minimum the reference checks against."""
+    from golden_io import acceptance_c1
+    for rec in acceptance_c1():
+        assert rec[64]["cost"] == rec["dag_cost"]
+        for prec in (32, 64):
+            o = O.linmdtw(rec["X"], rec["Y"], min_dim=2, precision=prec)
+            assert o["cost"] == rec[prec]["cost"]
+            assert np.array_equal(o["path"], rec[prec]["path"])
+            assert list(o["pivot_trace"]) == rec[prec]["trace"]
