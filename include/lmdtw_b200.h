@@ -208,6 +208,38 @@ int64_t lmdtw_peak_retained_values(int64_t kstop, int64_t M, int64_t N);
 /* Library-wide statistics: total kernels launched since load (for bench). */
 int64_t lmdtw_launch_count(void);
 
+/* ---- per-path steps either side of the aligner ---------- */
+
+/* approx.constrained_dtw (approx.py:180-220; fill _window_fill :130-177):
+ * optimal path among those inside the monotone staircase window
+ * lo[i] <= j <= hi[i] (M entries each, validated as approx.Window.validate,
+ * approx.py:52-63: EINVAL with the reference's messages).  path_out holds
+ * M+N-1 (i, j) pairs; *cells = window size (cells_processed).  A backtrace
+ * that meets SELF before (0, 0) returns EINTERNAL ("backtrace escaped the
+ * window"), the reference's RuntimeError. */
+int lmdtw_window_dtw(int device, const float *X, int64_t M, const float *Y, int64_t N, int32_t d,
+                     const int64_t *lo, const int64_t *hi, const int32_t tie[3], int32_t precision,
+                     int32_t mem, double *cost, int64_t *path_out, int64_t *path_len, int64_t *cells);
+
+/* core.frame_costs (core.py:167-179): out[q] = cost(A[q], B[q]) in
+ * `precision` (out is a host array of K floats or doubles). */
+int lmdtw_frame_costs(int device, const float *A, const float *B, int64_t K, int32_t d,
+                      int32_t precision, int32_t mem, void *out);
+
+/* core.path_cost (core.py:182-197) for npaths (X, Y, path) triples at once:
+ * per-cell costs in parallel, each path's sequential sum from 0 in
+ * `precision`; costs_out[p] as double.  X/Y per `mem`, paths on the host. */
+int lmdtw_path_cost_batch(int device, int32_t npaths, const float *const *X, const int64_t *M,
+                          const float *const *Y, const int64_t *N, int32_t d,
+                          const int64_t *const *paths, const int64_t *K, int32_t precision,
+                          int32_t mem, double *costs_out);
+
+/* metrics.discrepancy (metrics.py:44-63): errors_out[0..K1) row errors and
+ * errors_out[K1..2K1) column errors of path p1 against p2 (host arrays of
+ * (i, j) int64 pairs); EINVAL on mismatched endpoints. */
+int lmdtw_discrepancy(int device, const int64_t *p1, int64_t K1, const int64_t *p2, int64_t K2,
+                      int64_t *errors_out);
+
 #ifdef __cplusplus
 }
 #endif

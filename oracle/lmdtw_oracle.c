@@ -295,6 +295,66 @@ static int64_t solve_##SFX(const float *X, const float *Y, int64_t M, int64_t N,
     return nl + nr - 1;                                                                   \
 }                                                                                         \
                                                                                           \
+/* constrained_dtw (approx.py:180-220): _window_fill (approx.py:130-177) over rows     */   \
+/* lo[i]..hi[i], row-major, moves in tie order with strict <; no valid move -> inf    */   \
+/* and SELF; backtrace from the corner.  Returns the path length (path holds M+N-1   */   \
+/* pairs), -1 if the backtrace meets SELF early, -2 on OOM.                          */   \
+int64_t orc_window_dtw_##SFX(const float *X, const float *Y, int64_t M, int64_t N, int d,   \
+                             const int64_t *lo, const int64_t *hi, const int tie[3],        \
+                             double *cost_out, int64_t *path, int64_t *cells_out) {        \
+    int64_t *off = (int64_t *)malloc(sizeof(int64_t) * (M + 1));                          \
+    if (!off) return -2;                                                                  \
+    off[0] = 0;                                                                           \
+    for (int64_t i = 0; i < M; i++) off[i + 1] = off[i] + (hi[i] - lo[i] + 1);            \
+    T *D = (T *)malloc(sizeof(T) * off[M]);                                               \
+    uint8_t *P = (uint8_t *)malloc((size_t)off[M]);                                       \
+    if (!D || !P) { free(off); free(D); free(P); return -2; }                             \
+    for (int64_t i = 0; i < M; i++) {                                                     \
+        for (int64_t j = lo[i]; j <= hi[i]; j++) {                                        \
+            int64_t pos = off[i] + (j - lo[i]);                                           \
+            T c = cost_##SFX(X + i * (int64_t)d, Y + j * (int64_t)d, d);                   \
+            if (i == 0 && j == 0) { D[pos] = c; P[pos] = ORC_SELF; continue; }            \
+            T best = (T)0; int have = 0; int move = ORC_SELF;                             \
+            for (int m = 0; m < 3; m++) {                                                 \
+                int code = tie[m]; T v;                                                   \
+                if (code == ORC_LEFT) {                                                   \
+                    if (j - 1 < lo[i]) continue;                                          \
+                    v = D[pos - 1];                                                       \
+                } else if (code == ORC_UP) {                                              \
+                    if (i == 0 || j < lo[i - 1] || j > hi[i - 1]) continue;               \
+                    v = D[off[i - 1] + (j - lo[i - 1])];                                  \
+                } else {                                                                  \
+                    if (i == 0 || j - 1 < lo[i - 1] || j - 1 > hi[i - 1]) continue;       \
+                    v = D[off[i - 1] + (j - 1 - lo[i - 1])];                              \
+                }                                                                         \
+                if (!have || v < best) { best = v; move = code; have = 1; }               \
+            }                                                                             \
+            D[pos] = have ? best + c : (T)INFINITY;                                       \
+            P[pos] = (uint8_t)move;                                                       \
+        }                                                                                 \
+    }                                                                                     \
+    if (cost_out) *cost_out = (double)D[off[M] - 1];                                      \
+    if (cells_out) *cells_out = off[M];                                                   \
+    int64_t i = M - 1, j = N - 1, n = 0;                                                  \
+    path[0] = i; path[1] = j; n = 1;                                                      \
+    while (!(i == 0 && j == 0)) {                                                         \
+        int mv = P[off[i] + (j - lo[i])];                                                 \
+        if (mv == ORC_LEFT) j -= 1;                                                       \
+        else if (mv == ORC_UP) i -= 1;                                                    \
+        else if (mv == ORC_DIAG) { i -= 1; j -= 1; }                                      \
+        else { n = -1; break; }                                                           \
+        path[2 * n] = i; path[2 * n + 1] = j; n++;                                        \
+    }                                                                                     \
+    free(off); free(D); free(P);                                                          \
+    if (n < 0) return -1;                                                                 \
+    for (int64_t a = 0, b = n - 1; a < b; a++, b--) {                                     \
+        int64_t ti = path[2 * a], tj = path[2 * a + 1];                                   \
+        path[2 * a] = path[2 * b]; path[2 * a + 1] = path[2 * b + 1];                     \
+        path[2 * b] = ti; path[2 * b + 1] = tj;                                           \
+    }                                                                                     \
+    return n;                                                                             \
+}                                                                                         \
+                                                                                          \
 /* path_cost (core.py:182-197): per-cell costs in T, summed sequentially from 0.     */   \
 double orc_path_cost_##SFX(const float *X, const float *Y, int d, const int64_t *path,    \
                            int64_t K) {                                                   \

@@ -64,6 +64,9 @@ def lib():
             f = getattr(L, f"orc_find_pivot_{sfx}")
             f.argtypes = [P, P, I64, I64, I, I, P, P, P, P, P, P]
             f.restype = I
+            f = getattr(L, f"orc_window_dtw_{sfx}")
+            f.argtypes = [P, P, I64, I64, I, P, P, P, P, P, P]
+            f.restype = I64
             f = getattr(L, f"orc_path_cost_{sfx}")
             f.argtypes = [P, P, I, P, I64]
             f.restype = C.c_double
@@ -162,6 +165,23 @@ def find_pivot(X, Y, precision=64, pivot_tie_rule="lowest"):
         raise ValueError("too small for a pivot search")
     return dict(i=pi.value, j=pj.value, total_at_pivot=tot.value, diagonal_k=k.value,
                 cells=cells.value, peak=peak.value)
+
+
+def window_dtw(X, Y, lo, hi, tie_rule=("diag", "left", "up"), precision=64):
+    """Oracle constrained_dtw over the window lo/hi: (cost, path, cells)."""
+    X, Y = _f32(X), _f32(Y)
+    M, N, d = X.shape[0], Y.shape[0], X.shape[1]
+    lo = np.ascontiguousarray(lo, dtype=np.int64)
+    hi = np.ascontiguousarray(hi, dtype=np.int64)
+    path = np.empty((M + N - 1, 2), np.int64)
+    cost = C.c_double()
+    cells = C.c_int64()
+    tie = tie_codes(tie_rule)
+    n = getattr(lib(), f"orc_window_dtw_{_sfx(precision)}")(_ptr(X), _ptr(Y), M, N, d, _ptr(lo), _ptr(hi),
+                                                            _ptr(tie), C.byref(cost), _ptr(path), C.byref(cells))
+    if n < 0:
+        raise RuntimeError(f"oracle window_dtw failed ({n})")
+    return cost.value, path[:n].copy(), cells.value
 
 
 def path_cost(X, Y, path, precision=64):

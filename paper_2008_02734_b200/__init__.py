@@ -20,12 +20,17 @@ from .core import (
     euclidean_cost,
     frame_costs,
     path_cost,
+    path_costs,
     precision_dtype,
     require_valid_path,
     validate_path,
 )
+from .approx import (Window, coarsen, constrained_dtw, expand_window, fastdtw, mrmsdtw, project_path,
+                     window_from_path)
 from .diagonal import DiagBuffers, diag_cells, diag_dtw, diag_length, diag_to_grid, peak_retained_values
 from .divide import LinMdtwConfig, Pivot, align_batch, cells_ratio, find_pivot, linmdtw
+from .metrics import (DiscrepancyReport, discrepancy, merge_reports, proportion_below,
+                      proportion_below_frames)
 from .textbook import (
     DIAG,
     LEFT,
@@ -53,4 +58,7 @@ __all__ = [
     "diag_length", "diag_to_grid", "dtw_full", "euclidean_cost", "find_pivot", "frame_costs",
     "get_device", "linmdtw", "path_cost", "peak_retained_values", "precision_dtype",
     "require_valid_path", "set_device", "tie_codes", "validate_path",
+    "Window", "coarsen", "constrained_dtw", "expand_window", "fastdtw", "mrmsdtw", "project_path",
+    "window_from_path", "DiscrepancyReport", "discrepancy", "merge_reports", "proportion_below",
+    "proportion_below_frames", "path_costs",
 ]

@@ -47,6 +47,7 @@ EXPORTS = (
     "lmdtw_peak_retained_values", "lmdtw_launch_count", "lmdtw_pivot_nodes", "lmdtw_leaf_nodes",
     "lmdtw_pivot_combine", "lmdtw_half_pass_shard", "lmdtw_handoff_words", "lmdtw_strip_height",
     "lmdtw_ipc_alloc", "lmdtw_ipc_open", "lmdtw_ipc_close", "lmdtw_ipc_free", "lmdtw_fill_ones",
+    "lmdtw_window_dtw", "lmdtw_frame_costs", "lmdtw_path_cost_batch", "lmdtw_discrepancy",
 )
 
 _lib = None
@@ -106,6 +107,14 @@ def load():
     L.lmdtw_pivot_combine.restype = C.c_int
     L.lmdtw_path_cost.argtypes = [P, I64, P, I64, I32, P, I64, I32, P]
     L.lmdtw_path_cost.restype = C.c_int
+    L.lmdtw_window_dtw.argtypes = [C.c_int, P, I64, P, I64, I32, P, P, P, I32, I32, P, P, P, P]
+    L.lmdtw_window_dtw.restype = C.c_int
+    L.lmdtw_frame_costs.argtypes = [C.c_int, P, P, I64, I32, I32, I32, P]
+    L.lmdtw_frame_costs.restype = C.c_int
+    L.lmdtw_path_cost_batch.argtypes = [C.c_int, I32, P, P, P, P, I32, P, P, I32, I32, P]
+    L.lmdtw_path_cost_batch.restype = C.c_int
+    L.lmdtw_discrepancy.argtypes = [C.c_int, P, I64, P, I64, P]
+    L.lmdtw_discrepancy.restype = C.c_int
     for f in ("lmdtw_diag_length", "lmdtw_cells_upto", "lmdtw_peak_retained_values"):
         getattr(L, f).argtypes = [I64, I64, I64]
         getattr(L, f).restype = I64

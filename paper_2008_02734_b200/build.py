@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "liblmdtw_b200.so")
 OBJDIR = os.path.join(HERE, "_build")
-SOURCES = ["kernels.cu", "engine.cu"]
+SOURCES = ["kernels.cu", "window.cu", "engine.cu"]
 HEADERS = [os.path.join(CSRC, "lmdtw_internal.h"), os.path.join(INCLUDE, "lmdtw_b200.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

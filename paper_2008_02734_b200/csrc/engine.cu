@@ -122,6 +122,9 @@ struct Ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     DBuf xraw, yraw, xp, yp, passes, items, counter, out, bnd, pdesc, pout, pscratch, ldesc, bp, path, pcost, plen,
         lcost, tab, trace, lb, flags, istage;
+    // window.cu entry points (constrained DTW, path costs, discrepancy)
+    DBuf wlo, whi, woff, wbp, wbnd, wdesc, wcost, wpath, wpoff, wplen, pcells, pcost2, poffs, pxoff, pyoff, ppid,
+        pout2, dsc;
     HBuf h_passes, h_items, h_istage, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
     long long call_launches = 0;
     long long h2d = 0, d2h = 0;
@@ -1676,6 +1679,233 @@ int lmdtw_path_cost(const float* X, int64_t M, const float* Y, int64_t N, int32_
         }
         *cost = total;
     }
+    return LMDTW_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------ per-path steps (window.cu)
+namespace {
+// Raw float32 rows on the device: host rows copied into `buf`, device rows used in place.
+int stage_raw(Ctx& c, DBuf& buf, const float* src, int64_t rows, int d, int mem, const float** out) {
+    if (mem == LMDTW_MEM_DEVICE) {
+        *out = src;
+        return LMDTW_OK;
+    }
+    const size_t b = (size_t)std::max<int64_t>(rows, 1) * d * sizeof(float);
+    CU(buf.ensure(b));
+    CU(cudaMemcpyAsync(buf.p, src, (size_t)rows * d * sizeof(float), cudaMemcpyHostToDevice, c.st));
+    c.h2d += (long long)rows * d * sizeof(float);
+    *out = buf.as<float>();
+    return LMDTW_OK;
+}
+
+// approx.Window.validate (approx.py:52-63), same checks and messages.
+int validate_window(const int64_t* lo, const int64_t* hi, int64_t M, int64_t N) {
+    if (M < 1) return set_err(LMDTW_EINVAL, "window lo/hi length mismatch");
+    for (int64_t i = 0; i < M; i++)
+        if (lo[i] < 0 || hi[i] >= N || lo[i] > hi[i]) return set_err(LMDTW_EINVAL, "window intervals empty or out of range");
+    for (int64_t i = 1; i < M; i++)
+        if (lo[i] < lo[i - 1] || hi[i] < hi[i - 1]) return set_err(LMDTW_EINVAL, "window staircase not monotone");
+    if (lo[0] != 0 || hi[M - 1] != N - 1) return set_err(LMDTW_EINVAL, "window must contain (0,0) and (M-1,N-1)");
+    for (int64_t i = 1; i < M; i++)
+        if (lo[i] > hi[i - 1] + 1) return set_err(LMDTW_EINVAL, "window rows disconnected; no warping path fits");
+    return LMDTW_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int lmdtw_window_dtw(int device, const float* X, int64_t M, const float* Y, int64_t N, int32_t d,
+                     const int64_t* lo, const int64_t* hi, const int32_t tie[3], int32_t precision, int32_t mem,
+                     double* cost, int64_t* path_out, int64_t* path_len, int64_t* cells) {
+    TRY(validate_common(M, N, d, precision));
+    TRY(validate_tie(tie));
+    TRY(validate_window(lo, hi, M, N));
+    CtxLease c;
+    TRY(lease_ctx(device, c));
+    c->call_launches = 0;
+    c->h2d = c->d2h = 0;
+    const float *dX = nullptr, *dY = nullptr;
+    TRY(stage_raw(*c, c->xraw, X, M, d, mem, &dX));
+    TRY(stage_raw(*c, c->yraw, Y, N, d, mem, &dY));
+    // window rows, backpointer word offsets, pipeline width
+    std::vector<int32_t> lo32(M), hi32(M);
+    std::vector<int64_t> wo(M + 1);
+    int64_t ncell = 0, span = 0;
+    wo[0] = 0;
+    for (int64_t i = 0; i < M; i++) {
+        lo32[i] = (int32_t)lo[i];
+        hi32[i] = (int32_t)hi[i];
+        wo[i + 1] = wo[i] + (hi[i] >> 5) - (lo[i] >> 5) + 1;
+        ncell += hi[i] - lo[i] + 1;
+    }
+    for (int64_t g = 0; g * 32 < M; g++) span = std::max<int64_t>(span, hi[std::min(M - 1, 32 * g + 31)] - lo[32 * g] + 32);
+    // groups in flight: a group trails its predecessor by >= 32 steps
+    const int warps = (int)std::min<int64_t>(16, std::max<int64_t>(2, (span + 31) / 32 + 1));
+    const int W = precision == 32 ? 1 : 2;
+    const int64_t bnd_words = 2 * ((N + 1) & ~1LL) * W;
+    CU(c->wlo.ensure(M * sizeof(int32_t)));
+    CU(c->whi.ensure(M * sizeof(int32_t)));
+    CU(c->woff.ensure((M + 1) * sizeof(int64_t)));
+    CU(c->wbp.ensure((size_t)wo[M] * 8));
+    CU(c->wbnd.ensure((size_t)bnd_words * 8));
+    CU(c->wdesc.ensure(sizeof(BandDesc)));
+    CU(c->wcost.ensure(8));
+    CU(c->wpath.ensure((size_t)(M + N) * 2 * sizeof(int)));
+    CU(c->wpoff.ensure(sizeof(int64_t)));
+    CU(c->wplen.ensure(sizeof(int)));
+    BandDesc bd{};
+    bd.M = (int32_t)M;
+    bd.N = (int32_t)N;
+    const int64_t zero = 0;
+    CU(cudaMemcpyAsync(c->wlo.p, lo32.data(), M * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->whi.p, hi32.data(), M * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->woff.p, wo.data(), (M + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->wdesc.p, &bd, sizeof bd, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->wpoff.p, &zero, sizeof zero, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemsetAsync(c->wbnd.p, 0xFF, (size_t)bnd_words * 8, c->st));  // tag -1
+    const int tie_i[3] = {tie[0], tie[1], tie[2]};
+    CU(launch_band(precision, dX, dY, d, c->wdesc.as<BandDesc>(), 1, warps, c->wlo.as<int32_t>(),
+                   c->whi.as<int32_t>(), c->woff.as<int64_t>(), c->wbp.as<unsigned long long>(),
+                   c->wbnd.as<unsigned long long>(), c->wcost.p, tie_i, c->st));
+    CU(launch_band_backtrace(c->wdesc.as<BandDesc>(), 1, c->wlo.as<int32_t>(), c->woff.as<int64_t>(),
+                             c->wbp.as<unsigned long long>(), c->wpath.as<int>(), c->wpoff.as<int64_t>(),
+                             c->wplen.as<int>(), c->st));
+    c->call_launches += 2;
+    g_launches += 2;
+    int plen = 0;
+    double dcost = 0;
+    float fcost = 0;
+    std::vector<int> rev((size_t)(M + N) * 2);
+    CU(cudaMemcpyAsync(&plen, c->wplen.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    if (precision == 32)
+        CU(cudaMemcpyAsync(&fcost, c->wcost.p, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    else
+        CU(cudaMemcpyAsync(&dcost, c->wcost.p, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(rev.data(), c->wpath.p, rev.size() * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    c->prof_collect();
+    if (plen < 0) return set_err(LMDTW_EINTERNAL, "backtrace escaped the window; window was infeasible");
+    for (int q = 0; q < plen; q++) {
+        path_out[2 * q] = rev[2 * (plen - 1 - q)];
+        path_out[2 * q + 1] = rev[2 * (plen - 1 - q) + 1];
+    }
+    if (path_len) *path_len = plen;
+    if (cost) *cost = precision == 32 ? (double)fcost : dcost;
+    if (cells) *cells = ncell;
+    return LMDTW_OK;
+}
+
+int lmdtw_frame_costs(int device, const float* A, const float* B, int64_t K, int32_t d, int32_t precision,
+                      int32_t mem, void* out) {
+    if (precision != 32 && precision != 64) return set_err(LMDTW_EINVAL, "precision must be 32 or 64");
+    if (d < 1 || K < 0) return set_err(LMDTW_EINVAL, "bad frame count or dimension");
+    if (K == 0) return LMDTW_OK;
+    CtxLease c;
+    TRY(lease_ctx(device, c));
+    const float *dA = nullptr, *dB = nullptr;
+    TRY(stage_raw(*c, c->xraw, A, K, d, mem, &dA));
+    TRY(stage_raw(*c, c->yraw, B, K, d, mem, &dB));
+    const size_t esz = precision == 32 ? 4 : 8;
+    CU(c->pcost2.ensure((size_t)K * esz));
+    CU(launch_path_costs(precision, dA, dB, d, nullptr, K, nullptr, nullptr, nullptr, c->pcost2.p, c->st));
+    g_launches++;
+    CU(cudaMemcpyAsync(out, c->pcost2.p, (size_t)K * esz, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return LMDTW_OK;
+}
+
+int lmdtw_path_cost_batch(int device, int32_t npaths, const float* const* X, const int64_t* M,
+                          const float* const* Y, const int64_t* N, int32_t d, const int64_t* const* paths,
+                          const int64_t* K, int32_t precision, int32_t mem, double* costs_out) {
+    if (precision != 32 && precision != 64) return set_err(LMDTW_EINVAL, "precision must be 32 or 64");
+    if (npaths < 1 || d < 1) return set_err(LMDTW_EINVAL, "npaths must be >= 1 and d >= 1");
+    int64_t ncell = 0, xrows = 0, yrows = 0;
+    for (int p = 0; p < npaths; p++) {
+        if (K[p] < 1) return set_err(LMDTW_EINVAL, "empty path");
+        for (int64_t q = 0; q < K[p]; q++) {
+            const int64_t i = paths[p][2 * q], j = paths[p][2 * q + 1];
+            if (i < 0 || i >= M[p] || j < 0 || j >= N[p]) return set_err(LMDTW_EINVAL, "path index out of range");
+        }
+        ncell += K[p];
+        xrows += M[p];
+        yrows += N[p];
+    }
+    CtxLease c;
+    TRY(lease_ctx(device, c));
+    // features: concatenated raw rows (device inputs are gathered by copies)
+    CU(c->xraw.ensure((size_t)xrows * d * 4));
+    CU(c->yraw.ensure((size_t)yrows * d * 4));
+    std::vector<int64_t> xo(npaths), yo(npaths), off(npaths + 1);
+    std::vector<int32_t> pid((size_t)ncell);
+    std::vector<int64_t> cells((size_t)ncell * 2);
+    const cudaMemcpyKind kind = mem == LMDTW_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    int64_t xr = 0, yr = 0, w = 0;
+    for (int p = 0; p < npaths; p++) {
+        xo[p] = xr;
+        yo[p] = yr;
+        off[p] = w;
+        CU(cudaMemcpyAsync(c->xraw.as<float>() + xr * d, X[p], (size_t)M[p] * d * 4, kind, c->st));
+        CU(cudaMemcpyAsync(c->yraw.as<float>() + yr * d, Y[p], (size_t)N[p] * d * 4, kind, c->st));
+        xr += M[p];
+        yr += N[p];
+        memcpy(cells.data() + 2 * w, paths[p], (size_t)K[p] * 2 * sizeof(int64_t));
+        std::fill(pid.begin() + w, pid.begin() + w + K[p], p);
+        w += K[p];
+    }
+    off[npaths] = w;
+    const size_t esz = precision == 32 ? 4 : 8;
+    CU(c->pcells.ensure((size_t)ncell * 16));
+    CU(c->ppid.ensure((size_t)ncell * 4));
+    CU(c->pxoff.ensure((size_t)npaths * 8));
+    CU(c->pyoff.ensure((size_t)npaths * 8));
+    CU(c->poffs.ensure((size_t)(npaths + 1) * 8));
+    CU(c->pcost2.ensure((size_t)ncell * esz));
+    CU(c->pout2.ensure((size_t)npaths * 8));
+    CU(cudaMemcpyAsync(c->pcells.p, cells.data(), (size_t)ncell * 16, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->ppid.p, pid.data(), (size_t)ncell * 4, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->pxoff.p, xo.data(), (size_t)npaths * 8, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->pyoff.p, yo.data(), (size_t)npaths * 8, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->poffs.p, off.data(), (size_t)(npaths + 1) * 8, cudaMemcpyHostToDevice, c->st));
+    CU(launch_path_costs(precision, c->xraw.as<float>(), c->yraw.as<float>(), d, c->pcells.as<int64_t>(), ncell,
+                         c->pxoff.as<int64_t>(), c->pyoff.as<int64_t>(), c->ppid.as<int32_t>(), c->pcost2.p, c->st));
+    CU(launch_seq_sums(precision, c->pcost2.p, c->poffs.as<int64_t>(), npaths, c->pout2.as<double>(), c->st));
+    g_launches += 2;
+    CU(cudaMemcpyAsync(costs_out, c->pout2.p, (size_t)npaths * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return LMDTW_OK;
+}
+
+int lmdtw_discrepancy(int device, const int64_t* p1, int64_t K1, const int64_t* p2, int64_t K2,
+                      int64_t* errors_out) {
+    if (K1 < 1 || K2 < 1) return set_err(LMDTW_EINVAL, "path must be a nonempty (K, 2) index array");
+    if (p1[0] != p2[0] || p1[1] != p2[1] || p1[2 * (K1 - 1)] != p2[2 * (K2 - 1)] ||
+        p1[2 * (K1 - 1) + 1] != p2[2 * (K2 - 1) + 1])
+        return set_err(LMDTW_EINVAL, "paths have mismatched endpoints; not comparable");
+    const int64_t M = p1[2 * (K1 - 1)] + 1, N = p1[2 * (K1 - 1) + 1] + 1;
+    if (M < 1 || N < 1) return set_err(LMDTW_EINVAL, "path index out of range");
+    for (int64_t q = 0; q < K1; q++)
+        if (p1[2 * q] < 0 || p1[2 * q] >= M || p1[2 * q + 1] < 0 || p1[2 * q + 1] >= N)
+            return set_err(LMDTW_EINVAL, "path index out of range");
+    for (int64_t q = 0; q < K2; q++)
+        if (p2[2 * q] < 0 || p2[2 * q] >= M || p2[2 * q + 1] < 0 || p2[2 * q + 1] >= N)
+            return set_err(LMDTW_EINVAL, "path index out of range");
+    CtxLease c;
+    TRY(lease_ctx(device, c));
+    // dsc: p1 | p2 | scratch 2M+2N | errors 2 K1 (int64 each)
+    const size_t n64 = (size_t)(2 * K1 + 2 * K2 + 2 * M + 2 * N + 2 * K1);
+    CU(c->dsc.ensure(n64 * 8));
+    int64_t* d1 = c->dsc.as<int64_t>();
+    int64_t* d2 = d1 + 2 * K1;
+    long long* scr = reinterpret_cast<long long*>(d2 + 2 * K2);
+    long long* err = scr + 2 * M + 2 * N;
+    CU(cudaMemcpyAsync(d1, p1, (size_t)K1 * 16, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(d2, p2, (size_t)K2 * 16, cudaMemcpyHostToDevice, c->st));
+    CU(launch_discrepancy(d1, K1, d2, K2, M, N, scr, err, c->st));
+    g_launches += 6;
+    CU(cudaMemcpyAsync(errors_out, err, (size_t)K1 * 16, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
     return LMDTW_OK;
 }
 

@@ -135,6 +135,38 @@ cudaError_t launch_backtrace(int precision, DimPlan dp, const void* X, const voi
 cudaError_t launch_pad_cast(int precision, const float* src, int64_t rows, int d, int dp, void* dst,
                             cudaStream_t stream);
 int max_resident_warps(int precision, DimPlan dp, int leaf, int device);
+
+// ---- window.cu: windowed DP (approx._window_fill), path costs, discrepancy
+// One constrained_dtw problem: rows [0, M) of a monotone staircase window
+// lo[win_off + i] .. hi[win_off + i]; backpointer words of row i start at
+// bp_off + woff[win_off + i] and cover the 32-column words lo>>5 .. hi>>5.
+struct BandDesc {
+    int64_t x_off, y_off;   // first row in the raw float32 X / Y arrays
+    int32_t M, N;
+    int64_t win_off;        // offset into lo / hi / woff
+    int64_t bp_off;         // backpointer word offset
+    int64_t bnd_off;        // handoff words: 2 slots x N (x2 for fp64)
+    int32_t id;             // index of the D(M-1, N-1) output
+    int32_t pad;
+};
+cudaError_t launch_band(int precision, const float* X, const float* Y, int d, const BandDesc* probs, int nprobs,
+                        int warps, const int32_t* lo, const int32_t* hi, const int64_t* woff,
+                        unsigned long long* bp, unsigned long long* bnd, void* cost_out, const int tie[3],
+                        cudaStream_t stream);
+cudaError_t launch_band_backtrace(const BandDesc* probs, int nprobs, const int32_t* lo, const int64_t* woff,
+                                  const unsigned long long* bp, int* path, const int64_t* path_off, int* plen,
+                                  cudaStream_t stream);
+// per-cell costs of (X[x_off[p] + i], Y[y_off[p] + j]) for path cells (i, j);
+// cells == nullptr: row q of X against row q of Y
+cudaError_t launch_path_costs(int precision, const float* X, const float* Y, int d, const int64_t* cells,
+                              long long ncells, const int64_t* cell_xoff, const int64_t* cell_yoff,
+                              const int32_t* cell_path, void* costs, cudaStream_t stream);
+// sequential sums of costs[off[p] .. off[p+1]) in the accumulation dtype
+cudaError_t launch_seq_sums(int precision, const void* costs, const int64_t* off, int npaths, double* out,
+                            cudaStream_t stream);
+// scratch: 2M + 2N int64; err: 2 K1 int64 (row errors, then column errors)
+cudaError_t launch_discrepancy(const int64_t* p1, long long K1, const int64_t* p2, long long K2, long long M,
+                               long long N, long long* scratch, long long* err, cudaStream_t stream);
 cudaError_t set_watchdog_ns(unsigned long long ns);  // per device (current device)
 cudaError_t wait_stats(unsigned long long* cycles, unsigned long long* count, int reset);
 

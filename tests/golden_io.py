@@ -61,3 +61,22 @@ def acceptance_c1():
             rec[prec] = {"cost": float(z[f"cost{prec}"][q]), "path": path, "trace": trace}
         out.append(rec)
     return out
+
+
+_APPROX = None
+
+
+def approx_cases(prefix):
+    """Records of tests/golden/approx.npz (make_golden_approx.py) whose keys
+    start with `prefix` ("cw", "win", "fd", "md", "dc", "pc"); md/dc/pc records
+    share the index of the fd record built from the same inputs."""
+    global _APPROX
+    if _APPROX is None:
+        with np.load(os.path.join(GOLDEN, "approx.npz")) as f:
+            _APPROX = {k: f[k] for k in f.files}
+    count = int(_APPROX[("fd" if prefix in ("md", "dc", "pc") else prefix) + "_count"])
+    out = []
+    for q in range(count):
+        pre = f"{prefix}{q}/"
+        out.append({k[len(pre):]: v for k, v in _APPROX.items() if k.startswith(pre)})
+    return out

@@ -76,3 +76,14 @@ def test_acceptance_c1_sweep_oracle():
             assert o["cost"] == rec[prec]["cost"]
             assert np.array_equal(o["path"], rec[prec]["path"])
             assert list(o["pivot_trace"]) == rec[prec]["trace"]
+
+
+def test_window_dtw_matches_reference():
+    """Oracle constrained_dtw (approx.py:180-220) against the reference's
+    results on windows from window_from_path / expand_window / Window.full."""
+    from golden_io import approx_cases
+    for c in approx_cases("cw"):
+        cost, path, cells = O.window_dtw(c["X"], c["Y"], c["lo"], c["hi"], tie_rule(c["tie"]), int(c["prec"]))
+        assert cost == float(c["cost"])
+        assert np.array_equal(path, c["path"])
+        assert cells == int(c["cells"])
