@@ -146,6 +146,18 @@ __global__ void band_kernel(const float* __restrict__ X, const float* __restrict
             return Nm::get(bin + (long long)col * W, g - 1, v);
         };
         nok = load_blk(0, bnext);
+        // lane 0's first diagonal neighbour: row i0-1 at column B-1 (the feed
+        // starts at column B)
+        if (lane == 0 && need_col(B - 1)) {
+            const unsigned long long t0 = now_ns();
+            while (!Nm::get(bin + (long long)(B - 1) * W, g - 1, top_prev)) {
+                __nanosleep(64);
+                if (now_ns() - t0 > kBandWatchdogNs) {
+                    printf("lmdtw band watchdog: group %d corner stuck\n", g);
+                    __trap();
+                }
+            }
+        }
         for (int s = 0; s < nsteps; s++) {
             if ((s & 31) == 0) {
                 const int blk = s >> 5;
