@@ -165,6 +165,14 @@ int lmdtw_pivot_combine(int32_t precision, int64_t M, int64_t N, int32_t pivot_h
                         const void *const fwd_d[3], const void *const fwd_c[3],
                         const void *const bwd_d[3], int64_t *ijk, double *total);
 
+/* The same combine on `device` (pivot_kernel): the nine diagonals may be
+ * device pointers (e.g. NCCL all-gather outputs; lmdtw_half_pass and
+ * lmdtw_half_pass_shard accept device output pointers) or host pointers.
+ * Bit-identical to lmdtw_pivot_combine. */
+int lmdtw_pivot_combine_device(int device, int32_t precision, int64_t M, int64_t N, int32_t pivot_highest,
+                               const void *const fwd_d[3], const void *const fwd_c[3],
+                               const void *const bwd_d[3], int64_t *ijk, double *total);
+
 /* One shard of a half pass for the multi-GPU layout: strips
  * [strip_lo, strip_hi) of diag_dtw(X, Y, kstop, reverse), strips being
  * lmdtw_strip_height() grid rows.  bnd_local: caller-owned device buffer of

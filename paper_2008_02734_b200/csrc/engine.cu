@@ -1218,10 +1218,10 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
         const int64_t i0 = top - r1, cnt = r1 - r0 + 1;
         if (out_d && out_d[s3])
             CU(cudaMemcpyAsync((char*)out_d[s3] + i0 * E.esz, (char*)c->out.p + (pd.out_off[s3] + i0) * E.esz,
-                               cnt * E.esz, cudaMemcpyDeviceToHost, c->st));
+                               cnt * E.esz, cudaMemcpyDefault, c->st));
         if (out_c && out_c[s3])
             CU(cudaMemcpyAsync((char*)out_c[s3] + i0 * E.esz, (char*)c->out.p + (pd.out_off[3 + s3] + i0) * E.esz,
-                               cnt * E.esz, cudaMemcpyDeviceToHost, c->st));
+                               cnt * E.esz, cudaMemcpyDefault, c->st));
     }
     CU(cudaStreamSynchronize(c->st));
     c->prof_collect();
@@ -1419,10 +1419,10 @@ int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64
         const int64_t L = dlen(kstop - 2 + s, M, N);
         if (L > 0 && out_d && out_d[s])
             CU(cudaMemcpyAsync(out_d[s], (char*)c->out.p + P[0].out_off[s] * E.esz, L * E.esz,
-                               cudaMemcpyDeviceToHost, c->st));
+                               cudaMemcpyDefault, c->st));
         if (L > 0 && out_c && out_c[s])
             CU(cudaMemcpyAsync(out_c[s], (char*)c->out.p + P[0].out_off[3 + s] * E.esz, L * E.esz,
-                               cudaMemcpyDeviceToHost, c->st));
+                               cudaMemcpyDefault, c->st));
     }
     CU(cudaStreamSynchronize(c->st));
     c->prof_collect();
@@ -1620,6 +1620,75 @@ int lmdtw_pivot_combine(int32_t precision, int64_t M, int64_t N, int32_t pivot_h
         combine_pivot<float>(M, N, pivot_highest, fwd_d, fwd_c, bwd_d, ijk, total);
     else
         combine_pivot<double>(M, N, pivot_highest, fwd_d, fwd_c, bwd_d, ijk, total);
+    return LMDTW_OK;
+}
+
+// divide.find_pivot's combine (divide.py:122-145) on the device: the three
+// forward D and C diagonals and the three reverse D diagonals (device or host
+// pointers; host pointers are staged) are gathered into one device buffer and
+// reduced by pivot_kernel -- the multi-GPU path's combine after an NCCL
+// all-gather of the diagonals, bit-identical to lmdtw_pivot_combine.
+int lmdtw_pivot_combine_device(int device, int32_t precision, int64_t M, int64_t N, int32_t pivot_highest,
+                               const void* const fwd_d[3], const void* const fwd_c[3], const void* const bwd_d[3],
+                               int64_t* ijk, double* total) {
+    if (precision != 32 && precision != 64) return set_err(LMDTW_EINVAL, "precision must be 32 or 64");
+    if (M < 1 || N < 1 || M + N - 2 < 2) return set_err(LMDTW_EINVAL, "too small for a pivot search");
+    if (!fwd_d || !fwd_c || !bwd_d || !ijk || !total) return set_err(LMDTW_EINVAL, "null buffer");
+    CtxLease c;
+    TRY(lease_ctx(device, c));
+    const size_t esz = precision == 32 ? 4 : 8;
+    const int64_t K = M + N - 1, kf = (K + 1) / 2, kb = (K % 2 == 0) ? kf + 1 : kf;
+    PassDesc P[2] = {};
+    int64_t off = 0;
+    for (int s = 0; s < 3; s++) {  // fwd D, fwd C at kf-2+s; rev D at kb-2+s
+        P[0].out_off[s] = off;
+        off += dlen(kf - 2 + s, M, N);
+    }
+    for (int s = 0; s < 3; s++) {
+        P[0].out_off[3 + s] = off;
+        off += dlen(kf - 2 + s, M, N);
+    }
+    for (int s = 0; s < 3; s++) {
+        P[1].out_off[s] = off;
+        off += dlen(kb - 2 + s, M, N);
+    }
+    CU(c->out.ensure((size_t)std::max<int64_t>(off, 1) * esz));
+    for (int s = 0; s < 3; s++) {
+        const int64_t Lf = dlen(kf - 2 + s, M, N), Lb = dlen(kb - 2 + s, M, N);
+        if (Lf > 0) {
+            CU(cudaMemcpyAsync((char*)c->out.p + P[0].out_off[s] * esz, fwd_d[s], Lf * esz, cudaMemcpyDefault, c->st));
+            CU(cudaMemcpyAsync((char*)c->out.p + P[0].out_off[3 + s] * esz, fwd_c[s], Lf * esz, cudaMemcpyDefault,
+                               c->st));
+        }
+        if (Lb > 0)
+            CU(cudaMemcpyAsync((char*)c->out.p + P[1].out_off[s] * esz, bwd_d[s], Lb * esz, cudaMemcpyDefault, c->st));
+    }
+    PivotDesc v{};
+    v.fwd = 0;
+    v.bwd = 1;
+    v.M = (int32_t)M;
+    v.N = (int32_t)N;
+    v.kf = (int32_t)kf;
+    v.kb = (int32_t)kb;
+    v.highest = pivot_highest ? 1 : 0;
+    CU(c->passes.ensure(sizeof P));
+    CU(c->pdesc.ensure(sizeof v));
+    CU(c->pout.ensure(sizeof(PivotOut)));
+    CU(cudaMemcpyAsync(c->passes.p, P, sizeof P, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->pdesc.p, &v, sizeof v, cudaMemcpyHostToDevice, c->st));
+    const size_t scb = pivot_scratch_bytes(1);
+    CU(c->pscratch.ensure(scb));
+    CU(cudaMemsetAsync(c->pscratch.p, 0, scb, c->st));
+    CU(launch_pivots(precision, c->passes.as<PassDesc>(), c->pdesc.as<PivotDesc>(), 1, c->out.p,
+                     c->pout.as<PivotOut>(), c->pscratch.p, c->st));
+    g_launches++;
+    PivotOut po{};
+    CU(cudaMemcpyAsync(&po, c->pout.p, sizeof po, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    ijk[0] = po.i;
+    ijk[1] = po.j;
+    ijk[2] = po.k;
+    *total = po.total;
     return LMDTW_OK;
 }
 

@@ -26,7 +26,12 @@ The returned AlignmentResult (path, cost = core.path_cost, cells_processed,
 peak_diag_values, peak_table_cells, pivot_trace) is identical to
 divide.linmdtw's -- the partition never changes what is computed, only where.
 The only data-path exchange is pivots, half-pass diagonals and leaf paths
-(O(M + N) per level); features are replicated on every rank.
+(O(M + N) per level), moved by ``_exchange``: raw bytes in tensors through
+torch.distributed all_gather -- device tensors under NCCL, so diagonals go
+GPU to GPU and the split point is reduced on the device
+(lmdtw_pivot_combine_device); no pickling.  Features are replicated on every
+rank.  ``align_batch_distributed`` shards a batch of independent pairs
+(BASELINE cfg4) longest-first with no exchange but the results.
 
 The compute backend is pluggable: ``DeviceEngine`` drives the C ABI on this
 rank's GPU.  The CPU tests drive the same driver with a test engine to check
@@ -152,19 +157,24 @@ class DeviceEngine:
         i_off, j_off, M, N = sub
         kf, kb = _kstops(M, N)
         kstop = kb if reverse else kf
-        dt = np.float32 if self.prec == 32 else np.float64
         lens = [int(self.lib.lmdtw_diag_length(kstop - 2 + s, M, N)) for s in range(3)]
-        d = [np.empty(max(L, 1), dt) for L in lens]
-        c = [np.empty(max(L, 1), dt) for L in lens]
-        pd = (C.c_void_p * 3)(*[a.ctypes.data for a in d])
-        pc = (C.c_void_p * 3)(*[a.ctypes.data for a in c])
+        d = [self._dev_empty(L) for L in lens]
+        c = [self._dev_empty(L) for L in lens]
+        pd = (C.c_void_p * 3)(*[a.data_ptr() for a in d])
+        pc = (C.c_void_p * 3)(*[a.data_ptr() for a in c])
         cells = C.c_int64()
         Xs = self.Xd[i_off:i_off + M]
         Ys = self.Yd[j_off:j_off + N]
+        # outputs land in device tensors (the library copies with cudaMemcpyDefault)
         _capi.check(self.lib.lmdtw_half_pass(
             self.device, C.c_void_p(Xs.data_ptr()), M, C.c_void_p(Ys.data_ptr()), N, self.d, kstop,
             1 if reverse else 0, self.prec, _capi.MEM_DEVICE, pd, pc, C.byref(cells)))
         return [d[s][:lens[s]] for s in range(3)], [c[s][:lens[s]] for s in range(3)]
+
+    def _dev_empty(self, n):
+        import torch
+        dt = torch.float32 if self.prec == 32 else torch.float64
+        return torch.empty(max(int(n), 1), dtype=dt, device=f"cuda:{self.device}")
 
     def strip_height(self):
         return int(self.lib.lmdtw_strip_height(self.prec, self.d))
@@ -175,12 +185,11 @@ class DeviceEngine:
         i_off, j_off, M, N = sub
         kf, kb = _kstops(M, N)
         kstop = kb if reverse else kf
-        dt = np.float32 if self.prec == 32 else np.float64
         lens = [int(self.lib.lmdtw_diag_length(kstop - 2 + s, M, N)) for s in range(3)]
-        d = [np.empty(max(L, 1), dt) for L in lens]
-        c = [np.empty(max(L, 1), dt) for L in lens]
-        pd = (C.c_void_p * 3)(*[a.ctypes.data for a in d])
-        pc = (C.c_void_p * 3)(*[a.ctypes.data for a in c])
+        d = [self._dev_empty(L) for L in lens]
+        c = [self._dev_empty(L) for L in lens]
+        pd = (C.c_void_p * 3)(*[a.data_ptr() for a in d])
+        pc = (C.c_void_p * 3)(*[a.data_ptr() for a in c])
         cells = C.c_int64()
         Xs = self.Xd[i_off:i_off + M]
         Ys = self.Yd[j_off:j_off + N]
@@ -190,7 +199,7 @@ class DeviceEngine:
         out = {}
         for s3, (a, b) in enumerate(_shard_idx(kstop, M, N, lo, hi, self.strip_height())):
             if b > a:
-                out[s3] = (a, d[s3][a:b].copy(), c[s3][a:b].copy())
+                out[s3] = (a, d[s3][a:b].clone(), c[s3][a:b].clone())
         return out
 
     def handoff_alloc(self, nbytes):
@@ -215,14 +224,19 @@ class DeviceEngine:
         _capi.check(self.lib.lmdtw_ipc_free(self.device, ptr))
 
     def combine(self, M, N, fwd_d, fwd_c, bwd_d):
-        """Split point from the two halves (divide.py:122-145)."""
-        fd = (C.c_void_p * 3)(*[np.ascontiguousarray(a).ctypes.data for a in fwd_d])
-        fc = (C.c_void_p * 3)(*[np.ascontiguousarray(a).ctypes.data for a in fwd_c])
-        bd = (C.c_void_p * 3)(*[np.ascontiguousarray(a).ctypes.data for a in bwd_d])
+        """Split point from the two halves (divide.py:122-145), reduced on this
+        rank's GPU by pivot_kernel (lmdtw_pivot_combine_device); the
+        diagonals are device tensors after an NCCL exchange (host tensors
+        under gloo are staged by the library)."""
+        keep = [a.contiguous() for a in list(fwd_d) + list(fwd_c) + list(bwd_d)]
+        fd = (C.c_void_p * 3)(*[a.data_ptr() for a in keep[0:3]])
+        fc = (C.c_void_p * 3)(*[a.data_ptr() for a in keep[3:6]])
+        bd = (C.c_void_p * 3)(*[a.data_ptr() for a in keep[6:9]])
         ijk = np.zeros(3, np.int64)
         tot = C.c_double()
-        _capi.check(self.lib.lmdtw_pivot_combine(self.prec, M, N, 1 if self.cfg.pivot_tie_rule == "highest" else 0,
-                                                 fd, fc, bd, _capi.ptr(ijk), C.byref(tot)))
+        _capi.check(self.lib.lmdtw_pivot_combine_device(
+            self.device, self.prec, M, N, 1 if self.cfg.pivot_tie_rule == "highest" else 0, fd, fc, bd,
+            _capi.ptr(ijk), C.byref(tot)))
         return int(ijk[0]), int(ijk[1]), int(ijk[2]), float(tot.value)
 
     def leaves(self, subs):
@@ -254,18 +268,99 @@ class DeviceEngine:
         return float(cost.value)
 
 
-def _all_gather(obj, group):
+def _comm_device(group):
+    """Where exchanged tensors live: this rank's GPU under NCCL, host under gloo."""
+    import torch
     import torch.distributed as dist
-    out = [None] * dist.get_world_size(group)
-    dist.all_gather_object(out, obj, group=group)
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+_CODES = None
+
+
+def _exchange(mine, group):
+    """All-gather {int key: [1-D arrays]} from every rank without pickling:
+    each rank packs its arrays as raw bytes (8-byte aligned) into one uint8
+    tensor plus an int64 header (key, count, then dtype code and length per
+    array); sizes, headers and payloads go through dist.all_gather on the
+    communication device (GPU under NCCL -- diagonals move device to device).
+    Returns {key: [tensors on the communication device]} merged over ranks."""
+    import torch
+    import torch.distributed as dist
+    global _CODES
+    if _CODES is None:
+        _CODES = [torch.float32, torch.float64, torch.int64, torch.uint8]
+    dev = _comm_device(group)
+    hdr, parts = [], []
+    for key in sorted(mine):
+        arrs = mine[key]
+        hdr += [int(key), len(arrs)]
+        for a in arrs:
+            t = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(a))).reshape(-1)
+            t = t.to(dev).contiguous()
+            hdr += [_CODES.index(t.dtype), t.numel()]
+            b = t.view(torch.uint8)
+            parts.append(b)
+            if b.numel() % 8:
+                parts.append(torch.zeros(8 - b.numel() % 8, dtype=torch.uint8, device=dev))
+    world = dist.get_world_size(group)
+    h = torch.tensor(hdr, dtype=torch.int64, device=dev)
+    p = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.uint8, device=dev)
+    sz = torch.tensor([h.numel(), p.numel()], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(sz) for _ in range(world)]
+    dist.all_gather(sizes, sz, group=group)
+    sizes = [tuple(int(v) for v in x.tolist()) for x in sizes]
+    hmax = max(1, max(x[0] for x in sizes))
+    pmax = max(8, max(x[1] for x in sizes))
+    hp = torch.zeros(hmax, dtype=torch.int64, device=dev)
+    hp[:h.numel()] = h
+    pp = torch.zeros(pmax, dtype=torch.uint8, device=dev)
+    pp[:p.numel()] = p
+    hs = [torch.empty_like(hp) for _ in range(world)]
+    ps = [torch.empty_like(pp) for _ in range(world)]
+    dist.all_gather(hs, hp, group=group)
+    dist.all_gather(ps, pp, group=group)
+    out = {}
+    for r in range(world):
+        hr = hs[r][:sizes[r][0]].tolist()
+        q = o = 0
+        while q < len(hr):
+            key, n = hr[q], hr[q + 1]
+            q += 2
+            arrs = []
+            for _ in range(n):
+                dt, cnt = _CODES[hr[q]], hr[q + 1]
+                q += 2
+                nb = cnt * torch.empty(0, dtype=dt).element_size()
+                arrs.append(ps[r][o:o + nb].view(dt))
+                o += nb + (-nb) % 8
+            out[key] = arrs
     return out
+
+
+def _all_ok(ok, group):
+    """Every rank learns whether all ranks succeeded (one all_reduce MIN)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([1 if ok else 0], dtype=torch.int64, device=_comm_device(group))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item())
+
+
+def _host(a):
+    """Tensor or array -> numpy (host)."""
+    return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
 
 
 def _sharded_half_passes(engine, subs, units, weights, rank, world, group):
     """Fewer half passes than ranks: each gets a group of consecutive ranks and
     is cut into strip shards that run concurrently, shard j's first strip
     reading shard j-1's handoff buffer through CUDA IPC.  Returns
-    {unit: (d[3], c[3])} with the merged diagonals, on every rank."""
+    {unit: (d[3], c[3])} with the merged diagonals, on every rank.  A failure
+    on any rank is raised on every rank (collectives stay matched)."""
+    import torch
     import torch.distributed as dist
     H = engine.strip_height()
     alloc = apportion(world, weights)
@@ -285,11 +380,11 @@ def _sharded_half_passes(engine, subs, units, weights, rank, world, group):
     nmax = max(n for _, _, _, n in subs)
     nbytes = int(_capi.load().lmdtw_handoff_words(nmax, engine.prec)) * 8
     ptr, handle = engine.handoff_alloc(nbytes)
-    handles = _all_gather(handle, group)
+    handles = {k: bytes(_host(v[0]).tobytes())
+               for k, v in _exchange({rank: [np.frombuffer(handle, np.uint8)]}, group).items()}
     engine.handoff_reset(ptr, nbytes)
     dist.barrier(group)  # every buffer reads tag -1 before any shard runs
-    peer = None
-    out = {}
+    peer, out, err = None, {}, None
     try:
         if rank in plan:
             u, j, lo, hi = plan[rank]
@@ -297,25 +392,34 @@ def _sharded_half_passes(engine, subs, units, weights, rank, world, group):
             if j > 0:
                 peer = engine.handoff_open(handles[shards_of[u][j - 1]])
                 prev = peer
-            out = {u: engine.half_pass_shard(subs[units[u][0]], units[u][1], lo, hi, ptr, prev)}
-        parts = _all_gather(out, group)
-    finally:
-        dist.barrier(group)  # no shard still reads a peer buffer
-        if peer is not None:
-            engine.handoff_close(peer)
-        engine.handoff_free(ptr)
+            for s3, (a, sd, sc) in engine.half_pass_shard(subs[units[u][0]], units[u][1], lo, hi, ptr,
+                                                           prev).items():
+                out[3 * u + s3] = [np.array([a], np.int64), sd, sc]
+    except Exception as e:  # noqa: BLE001 -- re-raised below, after the collective
+        err = e
+    ok = _all_ok(err is None, group)
+    parts = _exchange(out, group) if ok else {}
+    dist.barrier(group)  # no shard still reads a peer buffer
+    if peer is not None:
+        engine.handoff_close(peer)
+    engine.handoff_free(ptr)
+    if not ok:
+        raise err if err is not None else RuntimeError("a sharded half pass failed on another rank")
+    dev = _comm_device(group)
+    dt = torch.float32 if engine.prec == 32 else torch.float64
     got = {}
-    dt = np.float32 if engine.prec == 32 else np.float64
     for u, (q, rev) in enumerate(units):
         _, _, m, n = subs[q]
         kstop = _kstops(m, n)[rev]
         lens = [int(_capi.load().lmdtw_diag_length(kstop - 2 + s3, m, n)) for s3 in range(3)]
-        d = [np.full(L, np.nan, dt) for L in lens]
-        c = [np.full(L, np.nan, dt) for L in lens]
-        for part in parts:
-            for s3, (a, sd, sc) in part.get(u, {}).items():
-                d[s3][a:a + len(sd)] = sd
-                c[s3][a:a + len(sc)] = sc
+        d = [torch.full((L,), float("nan"), dtype=dt, device=dev) for L in lens]
+        c = [torch.full((L,), float("nan"), dtype=dt, device=dev) for L in lens]
+        for s3 in range(3):
+            if 3 * u + s3 in parts:
+                a_t, sd, sc = parts[3 * u + s3]
+                a = int(a_t[0])
+                d[s3][a:a + sd.numel()] = sd
+                c[s3][a:a + sc.numel()] = sc
         got[u] = (d, c)
     return got
 
@@ -363,10 +467,12 @@ def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | N
             owner = lpt_assign(w, world)
             mine = [q for q in range(len(subs)) if owner[q] == rank]
             res = engine.pivot_nodes([subs[q] for q in mine])
-            got = {}
-            for part in _all_gather(list(zip(mine, res)), group):
-                got.update(dict(part))
-            piv = [got[q] for q in range(len(subs))]
+            got = _exchange({q: [np.array(v[:3], np.int64), np.array([v[3]], np.float64)]
+                             for q, v in zip(mine, res)}, group)
+            piv = []
+            for q in range(len(subs)):
+                ijk, tot = _host(got[q][0]), _host(got[q][1])
+                piv.append((int(ijk[0]), int(ijk[1]), int(ijk[2]), float(tot[0])))
         else:
             # forward and reverse half passes as separate units
             units = [(q, rev) for q in range(len(subs)) for rev in (0, 1)]
@@ -374,10 +480,11 @@ def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | N
             if len(units) >= world or not hasattr(engine, "half_pass_shard"):
                 owner = lpt_assign(w, world)
                 mine = [u for u in range(len(units)) if owner[u] == rank]
-                res = {u: engine.half_pass(subs[units[u][0]], units[u][1]) for u in mine}
-                got = {}
-                for part in _all_gather(res, group):
-                    got.update(part)
+                res = {}
+                for u in mine:
+                    d, c = engine.half_pass(subs[units[u][0]], units[u][1])
+                    res[u] = list(d) + list(c)
+                got = {u: (v[:3], v[3:]) for u, v in _exchange(res, group).items()}
             else:
                 got = _sharded_half_passes(engine, subs, units, w, rank, world, group)
             piv = []
@@ -403,9 +510,9 @@ def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | N
     lsubs = [tuple(nodes[q][:4]) for q in leaves]
     owner = lpt_assign([m * n for _, _, m, n in lsubs], world)
     mine = [q for q in range(len(lsubs)) if owner[q] == rank]
-    got = {}
-    for part in _all_gather(dict(zip(mine, engine.leaves([lsubs[q] for q in mine]))), group):
-        got.update(part)
+    got = {q: _host(v[0]).reshape(-1, 2)
+           for q, v in _exchange(dict(zip(mine, ([p] for p in engine.leaves([lsubs[q] for q in mine])))),
+                                 group).items()}
 
     # pre-order DFS: pivot trace and leaf sequence (divide.py:160-178)
     trace, seq, stack = [], [], [0]
@@ -430,3 +537,49 @@ def linmdtw_distributed(X, Y, cost: str = "euclidean", config: LinMdtwConfig | N
         cost=engine.path_cost(path), path=path, cells_processed=int(cells), cells_budget=2 * M * N,
         precision=str(dtype), algorithm="linmdtw", peak_diag_values=int(peak_diag),
         peak_table_cells=int(peak_table), pivot_trace=tuple(trace))
+
+
+def align_batch_distributed(pairs, cost: str = "euclidean", config: LinMdtwConfig | None = None, group=None,
+                            aligner=None, **overrides) -> list:
+    """divide.align_batch over the ranks of ``group`` (BASELINE cfg4 sharded,
+    SURVEY.md 8(e) row 1): pairs are independent, so each rank aligns the
+    pairs LPT assigns it (longest first by M*N) in one fused batch on its GPU,
+    and the results (path, cost, counters, pivot trace) are exchanged so every
+    rank returns the full list in input order.  ``aligner(pairs, config)``
+    replaces the local compute (default: align_batch on this rank's GPU)."""
+    import torch.distributed as dist
+    from .divide import align_batch
+    check_cost_kind(cost)
+    cfg = config or LinMdtwConfig(**overrides)
+    if config is not None and overrides:
+        raise InvalidInputError("pass either a config object or keyword overrides, not both")
+    series = [(as_series(X), as_series(Y)) for X, Y in pairs]
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    owner = lpt_assign([len(X) * len(Y) for X, Y in series], world)
+    mine = [q for q in range(len(series)) if owner[q] == rank]
+    run = aligner or (lambda ps, c: align_batch(ps, config=c))
+    local = run([series[q] for q in mine], cfg) if mine else []
+    keys = ("i", "j", "i_off", "j_off", "M", "N", "sub_i", "sub_j", "diagonal_k")
+    pack = {}
+    for q, r in zip(mine, local):
+        tr = np.array([[e[k] for k in keys] for e in r.pivot_trace], np.int64).reshape(-1, len(keys))
+        pack[q] = [np.asarray(r.path, np.int64), np.array([r.cost], np.float64),
+                   np.array([r.cells_processed, r.cells_budget, r.peak_diag_values, r.peak_table_cells], np.int64),
+                   tr, np.array([e["total_at_pivot"] for e in r.pivot_trace], np.float64)]
+    got = _exchange(pack, group)
+    dtype = precision_dtype(cfg.precision)
+    out = []
+    for q in range(len(series)):
+        path, c, ints, tr, tots = (_host(a) for a in got[q])
+        trace = []
+        for row, t in zip(tr.reshape(-1, len(keys)), tots):
+            e = {k: int(v) for k, v in zip(keys, row)}
+            e["total_at_pivot"] = float(t)
+            trace.append(e)
+        out.append(AlignmentResult(
+            cost=float(c[0]), path=path.reshape(-1, 2).copy(), cells_processed=int(ints[0]),
+            cells_budget=int(ints[1]), precision=str(dtype), algorithm="linmdtw",
+            peak_diag_values=int(ints[2]), peak_table_cells=int(ints[3]),
+            pivot_trace=tuple({k: e[k] for k in ("i", "j", "i_off", "j_off", "M", "N", "sub_i", "sub_j",
+                                                   "total_at_pivot", "diagonal_k")} for e in trace)))
+    return out

@@ -204,3 +204,61 @@ def test_strip_ranges_and_apportion():
                 a, b = _shard_idx(kstop, M, N, lo, hi, H)[s3]
                 seen[a:b] += 1
             assert np.all(seen == 1)
+
+
+def _batch_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2008_02734_b200.distributed import align_batch_distributed
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pairs = [_pair(int(m), int(n), 3, 50 + t) for t, (m, n) in
+                 enumerate(np.random.default_rng(4).integers(40, 400, size=(7, 2)))]
+        done = []
+
+        def oracle_batch(ps, cfg):  # test-only local compute: the C oracle per pair
+            out = []
+            for X, Y in ps:
+                done.append((len(X), len(Y)))
+                o = O.linmdtw(X.frames, Y.frames, min_dim=cfg.min_dim, precision=cfg.precision)
+                out.append(L.AlignmentResult(
+                    cost=o["cost"], path=o["path"], cells_processed=o["cells_processed"],
+                    cells_budget=2 * len(X) * len(Y), precision="float32", algorithm="linmdtw",
+                    peak_diag_values=o["peak_diag_values"], peak_table_cells=o["peak_table_cells"],
+                    pivot_trace=o["pivot_trace"]))
+            return out
+
+        res = align_batch_distributed(pairs, min_dim=24, precision=32, aligner=oracle_batch)
+        q.put((rank, [(r.cost, r.path, r.cells_processed, r.peak_diag_values, r.peak_table_cells,
+                       list(r.pivot_trace)) for r in res], done))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_align_batch_distributed_gloo_world2():
+    """BASELINE cfg4's multi-GPU sharding (pairs LPT-assigned to ranks, results
+    exchanged as raw tensors): every rank returns every pair's result, equal
+    to the single-process oracle, and each pair was aligned exactly once."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        rank, res, done = q.get(timeout=300)
+        got[rank] = (res, done)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pairs = [_pair(int(m), int(n), 3, 50 + t) for t, (m, n) in
+             enumerate(np.random.default_rng(4).integers(40, 400, size=(7, 2)))]
+    assert sorted(got[0][1] + got[1][1]) == sorted((len(X), len(Y)) for X, Y in pairs)
+    for rank in (0, 1):
+        for (X, Y), (cost, path, cells, pkd, pkt, trace) in zip(pairs, got[rank][0]):
+            o = O.linmdtw(X, Y, min_dim=24, precision=32)
+            assert cost == o["cost"] and np.array_equal(path, o["path"])
+            assert cells == o["cells_processed"] and pkd == o["peak_diag_values"] and pkt == o["peak_table_cells"]
+            assert trace == list(o["pivot_trace"])

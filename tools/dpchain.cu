@@ -195,12 +195,84 @@ template <int R, int SKEW> void run(const float* c, float* o, long long* cy, int
   printf("R=%d skew=%d burners/SMSP=%d: %.1f cyc/step  %.3f cells/cyc/warp\n", R, SKEW, burners / 4, per,
          32.0 * R / per);
 }
+
+// "Split" step: the lane's top-independent part X_r (its rows' values if the
+// row above contributed +inf) is computed from the previous step's values
+// while the shuffle is in flight; the chain from the arriving top is only
+// t_r = (((top + c0) + c1) ...) and D_r = min(X_r, t_r) -- exact because
+// rounding is monotone: fl(min(a, b) + c) = min(fl(a + c), fl(b + c)).
+template <int R>
+__device__ void dps(const float* __restrict__ cin, float* out, int steps, long long* cyc) {
+  const int lane = threadIdx.x & 31;
+  float L[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) L[r] = 1e30f;
+  float bottom = 1e30f, prevtop = 0.f;
+  const float feedv = 0.5f + lane;
+  float cn[R];
+#pragma unroll
+  for (int q = 0; q < R / 4; q++) {
+    const float4 c = reinterpret_cast<const float4*>(cin)[(lane) * (R / 4) + q];
+    cn[4 * q] = c.x; cn[4 * q + 1] = c.y; cn[4 * q + 2] = c.z; cn[4 * q + 3] = c.w;
+  }
+  long long t0 = clock64();
+#pragma unroll 4
+  for (int s = 0; s < steps; s++) {
+    float cc[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) cc[r] = cn[r];
+#pragma unroll
+    for (int q = 0; q < R / 4; q++) {
+      const float4 c = reinterpret_cast<const float4*>(cin)[(((s + 1) & 63) * 32 + lane) * (R / 4) + q];
+      cn[4 * q] = c.x; cn[4 * q + 1] = c.y; cn[4 * q + 2] = c.z; cn[4 * q + 3] = c.w;
+    }
+    const float feed = __shfl_sync(0xffffffffu, feedv, s & 31);
+    float top = __shfl_sync(0xffffffffu, bottom, (lane + 31) & 31);
+    // off the cross-lane chain
+    float X[R];
+    float dg = prevtop;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const float a = __fadd_rn(mn(L[r], dg), cc[r]);
+      X[r] = r == 0 ? a : mn(a, __fadd_rn(X[r - 1], cc[r]));
+      dg = L[r];
+    }
+    top = lane == 0 ? feed : top;
+    float t = top;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      t = __fadd_rn(t, cc[r]);
+      L[r] = mn(X[r], t);
+    }
+    bottom = L[R - 1];
+    prevtop = top;
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = bottom;
+  if (lane == 0) cyc[threadIdx.x >> 5] = t1 - t0;
+}
+template <int R>
+__global__ void ks(const float* cin, float* out, int steps, long long* cyc, int burners) {
+  const int w = threadIdx.x >> 5;
+  if (w >= burners) dps<R>(cin, out, steps, cyc);
+  else burn(out, steps * R / 2);
+}
+template <int R> void runs(const float* c, float* o, long long* cy, int burners) {
+  const int steps = 20000;
+  ks<R><<<1, 32 * (burners + 4)>>>(c, o, steps, cy, burners);
+  cudaDeviceSynchronize();
+  long long h[32];
+  cudaMemcpy(h, cy, sizeof(h), cudaMemcpyDeviceToHost);
+  const double per = (double)h[burners] / steps;
+  printf("SPLIT R=%d burners/SMSP=%d: %.1f cyc/step  %.3f cells/cyc/warp\n", R, burners / 4, per, 32.0 * R / per);
+}
 int main() {
   float* c; cudaMalloc(&c, 64 * 32 * 8 * 4); cudaMemset(c, 0, 64 * 32 * 8 * 4);
   float* o; cudaMalloc(&o, 4096); long long* cy; cudaMalloc(&cy, 256);
-  for (int b : {0, 12}) {
+  for (int b : {0, 4, 8, 12}) {
     run<4, 1>(c, o, cy, b); run<4, 2>(c, o, cy, b);
     run<8, 1>(c, o, cy, b); run<8, 2>(c, o, cy, b);
+    runs<4>(c, o, cy, b); runs<8>(c, o, cy, b);
     runc<2, 1>(c, o, cy, b); runc<2, 2>(c, o, cy, b); runc<4, 1>(c, o, cy, b); runc<4, 2>(c, o, cy, b);
     const int steps = 20000;
     k2<<<1, 32 * (b + 4)>>>(c, o, steps, cy, b);
