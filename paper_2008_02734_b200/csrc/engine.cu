@@ -115,17 +115,28 @@ struct HBuf {
     template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// One in-flight batch of half passes (a set of recursion nodes): its stream
+// and its buffers.  Batches run concurrently on their own streams, so the
+// children of a node start while other nodes of its level still run.
+struct Slot {
+    cudaStream_t st = nullptr;
+    cudaEvent_t done = nullptr;
+    DBuf passes, items, counter, out, bnd, pdesc, pout, pscratch, trace, lb, flags, istage;
+    HBuf h_passes, h_items, h_istage, h_pdesc, h_pout;
+};
+
 struct Ctx {
     int device = 0;
     std::mutex mu;
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    DBuf xraw, yraw, xp, yp, passes, items, counter, out, bnd, pdesc, pout, pscratch, ldesc, bp, path, pcost, plen,
-        lcost, tab, trace, lb, flags, istage;
+    Slot main;                                  // main.st == st
+    std::vector<std::unique_ptr<Slot>> extra;   // more batch slots, created on demand
+    DBuf xraw, yraw, xp, yp, ldesc, bp, path, pcost, plen, lcost, tab;
     // window.cu entry points (constrained DTW, path costs, discrepancy)
     DBuf wlo, whi, woff, wbp, wbnd, wdesc, wcost, wpath, wpoff, wplen, pcells, pcost2, poffs, pxoff, pyoff, ppid,
         pout2, dsc;
-    HBuf h_passes, h_items, h_istage, h_pdesc, h_pout, h_path, h_pcost, h_plen, h_lcost;
+    HBuf h_path, h_pcost, h_plen, h_lcost;
     long long call_launches = 0;
     long long h2d = 0, d2h = 0;
     // profiling (lmdtw_profile_enable): events around wave launches, read
@@ -157,21 +168,51 @@ void Ctx::prof_collect() {
         ev_used = 0;
         return;
     }
-    std::lock_guard<std::mutex> g(g_stats.mu);
+    // Launches of concurrent batches overlap: the time charged to waves and
+    // to leaves is the union of their [start, end] intervals, measured from
+    // the first pending event.
+    std::vector<std::pair<float, float>> waves, leaves;
+    long long wcells = 0, lcells = 0, wl = 0;
+    const cudaEvent_t ref = evpool[pend[0].e0];
     for (const Pend& p : pend) {
-        float ms = 0;
-        if (cudaEventElapsedTime(&ms, evpool[p.e0], evpool[p.e1]) != cudaSuccess) {
+        float a = 0, b = 0;
+        if (cudaEventElapsedTime(&a, ref, evpool[p.e0]) != cudaSuccess ||
+            cudaEventElapsedTime(&b, ref, evpool[p.e1]) != cudaSuccess) {
             cudaGetLastError();
             continue;
         }
         if (p.leaf) {
-            g_stats.leaf_ms += ms;
-            g_stats.leaf_cells += p.cells;
+            leaves.emplace_back(a, b);
+            lcells += p.cells;
         } else {
-            g_stats.wave_ms += ms;
-            g_stats.wave_launches += 1;
-            g_stats.wave_cells += p.cells;
+            waves.emplace_back(a, b);
+            wcells += p.cells;
+            wl++;
         }
+    }
+    auto span = [](std::vector<std::pair<float, float>>& v) {
+        std::sort(v.begin(), v.end());
+        double tot = 0, lo = 0, hi = -1e30;
+        for (auto& iv : v) {
+            if (iv.first > hi) {
+                if (hi > lo) tot += hi - lo;
+                lo = iv.first;
+                hi = iv.second;
+            } else {
+                hi = std::max<double>(hi, iv.second);
+            }
+        }
+        if (hi > lo) tot += hi - lo;
+        return tot;
+    };
+    const double wms = span(waves), lms = span(leaves);
+    {
+        std::lock_guard<std::mutex> g(g_stats.mu);
+        g_stats.wave_ms += wms;
+        g_stats.wave_launches += wl;
+        g_stats.wave_cells += wcells;
+        g_stats.leaf_ms += lms;
+        g_stats.leaf_cells += lcells;
     }
     pend.clear();
     ev_used = 0;
@@ -198,6 +239,8 @@ int make_ctx(int device, std::unique_ptr<Ctx>& out) {
     CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     CU(cudaEventCreate(&c->ev0));
     CU(cudaEventCreate(&c->ev1));
+    c->main.st = c->st;
+    CU(cudaEventCreateWithFlags(&c->main.done, cudaEventDisableTiming));
     if (const char* w = getenv("LMDTW_WATCHDOG_S")) {
         const double sec = atof(w);  // 0 disables the watchdog
         if (sec >= 0) CU(set_watchdog_ns((unsigned long long)(sec * 1e9)));
@@ -337,6 +380,7 @@ struct Node {
     int64_t pi = -1, pj = -1, k = -1;
     double total = 0;
     int leaf = -1;  // index into leaf list
+    int depth = 0;  // recursion level (root 0)
 };
 
 struct Engine {
@@ -414,7 +458,7 @@ struct Engine {
     // exclusive prefix sum is each key's first queue slot.  The tiles
     // themselves are scattered on the device (scatter_items_kernel), so the
     // host never touches the O(tiles) queue.  Returns the number of tiles.
-    int64_t stage_items(const std::vector<PassDesc>& P, int64_t& nents, int64_t& nkeys) {
+    int64_t stage_items(Slot& S, const std::vector<PassDesc>& P, int64_t& nents, int64_t& nkeys) {
         static_assert(kTileW % kLagKey == 0, "tile width must be a multiple of the key lag");
         constexpr int64_t kPer = kTileW / kLagKey;
         int64_t mmax = 0, total = 0;
@@ -429,9 +473,9 @@ struct Engine {
         }
         nkeys = mmax + 1;
         const size_t ent_bytes = (size_t)nents * sizeof(StripEnt);
-        CU(c.h_istage.ensure(ent_bytes + (size_t)(nkeys + kPer) * sizeof(int32_t)));
-        StripEnt* ents = c.h_istage.as<StripEnt>();
-        int32_t* cnt = reinterpret_cast<int32_t*>(c.h_istage.as<char>() + ent_bytes);
+        CU(S.h_istage.ensure(ent_bytes + (size_t)(nkeys + kPer) * sizeof(int32_t)));
+        StripEnt* ents = S.h_istage.as<StripEnt>();
+        int32_t* cnt = reinterpret_cast<int32_t*>(S.h_istage.as<char>() + ent_bytes);
         std::fill(cnt, cnt + nkeys + kPer, 0);
         int64_t e = 0;
         for (size_t q = 0; q < P.size(); q++)
@@ -452,29 +496,29 @@ struct Engine {
         return total;
     }
 
-    // Build the tile queue of passes P in c.items (device), on c.st.
-    int upload_queue(const std::vector<PassDesc>& P, int64_t& nitems) {
+    // Build the tile queue of passes P in S.items (device), on c.st.
+    int upload_queue(Slot& S, const std::vector<PassDesc>& P, int64_t& nitems) {
         int64_t nents = 0, nkeys = 0;
-        nitems = stage_items(P, nents, nkeys);
+        nitems = stage_items(S, P, nents, nkeys);
         if (nitems < 0 || nitems > INT32_MAX) return set_err(LMDTW_EINTERNAL, "tile queue size");
         const size_t ent_bytes = (size_t)nents * sizeof(StripEnt);
         const size_t stage_bytes = ent_bytes + (size_t)nkeys * sizeof(int32_t);
-        CU(c.items.ensure((size_t)std::max<int64_t>(nitems, 1) * sizeof(WorkItem)));
-        CU(c.istage.ensure(stage_bytes));
-        CU(cudaMemcpyAsync(c.istage.p, c.h_istage.p, stage_bytes, cudaMemcpyHostToDevice, c.st));
-        return launched(launch_scatter_items(c.istage.as<StripEnt>(), (int)nents,
-                                             reinterpret_cast<int32_t*>(c.istage.as<char>() + ent_bytes),
-                                             (int)(kTileW / kLagKey), c.items.as<WorkItem>(), c.st),
+        CU(S.items.ensure((size_t)std::max<int64_t>(nitems, 1) * sizeof(WorkItem)));
+        CU(S.istage.ensure(stage_bytes));
+        CU(cudaMemcpyAsync(S.istage.p, S.h_istage.p, stage_bytes, cudaMemcpyHostToDevice, S.st));
+        return launched(launch_scatter_items(S.istage.as<StripEnt>(), (int)nents,
+                                             reinterpret_cast<int32_t*>(S.istage.as<char>() + ent_bytes),
+                                             (int)(kTileW / kLagKey), S.items.as<WorkItem>(), S.st),
                         "scatter_items_kernel");
     }
 
     // Host-built queue (debug entry points only): same order as the device
     // scatter up to the order of tiles that share a key.
-    void make_items(const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
+    void make_items(Slot& S, const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
         constexpr int64_t kPer = kTileW / kLagKey;
         int64_t nents = 0, nkeys = 0;
-        const int64_t total = stage_items(P, nents, nkeys);
-        std::vector<int32_t> cur(c.h_istage.as<int32_t>() + nents * 3, c.h_istage.as<int32_t>() + nents * 3 + nkeys);
+        const int64_t total = stage_items(S, P, nents, nkeys);
+        std::vector<int32_t> cur(S.h_istage.as<int32_t>() + nents * 3, S.h_istage.as<int32_t>() + nents * 3 + nkeys);
         items.resize(std::max<int64_t>(total, 0));
         for (size_t q = 0; q < P.size(); q++)
             for (int a = P[q].strip_lo; a < P[q].strip_hi; a++)
@@ -482,7 +526,7 @@ struct Engine {
                     items[cur[b * kPer + a]++] = WorkItem{(int)q, a, (int)b, 0};
     }
 
-    int run_wave(const std::vector<PassDesc>& P0, int64_t bnd_total, bool leaf, void* tab, void* lcost,
+    int run_wave(Slot& S, const std::vector<PassDesc>& P0, int64_t bnd_total, bool leaf, void* tab, void* lcost,
                  int64_t cells) {
         const auto th0 = std::chrono::steady_clock::now();
         // tile bookkeeping: per strip H+1 boundary values and a completion count
@@ -495,33 +539,33 @@ struct Engine {
             lb_total += (int64_t)p.nstrips * (H + 1);
             flag_total += p.nstrips;
         }
-        CU(c.lb.ensure((size_t)std::max<int64_t>(lb_total, 1) * esz));
-        CU(c.flags.ensure((size_t)std::max<int64_t>(flag_total, 1) * sizeof(int)));
-        CU(cudaMemsetAsync(c.flags.p, 0, (size_t)std::max<int64_t>(flag_total, 1) * sizeof(int), c.st));
-        CU(c.h_passes.ensure(P.size() * sizeof(PassDesc)));
-        memcpy(c.h_passes.p, P.data(), P.size() * sizeof(PassDesc));
-        CU(c.passes.ensure(P.size() * sizeof(PassDesc)));
-        CU(c.counter.ensure(sizeof(int)));
-        CU(c.bnd.ensure((size_t)bnd_total * 8));
-        CU(cudaMemcpyAsync(c.passes.p, c.h_passes.p, P.size() * sizeof(PassDesc), cudaMemcpyHostToDevice, c.st));
+        CU(S.lb.ensure((size_t)std::max<int64_t>(lb_total, 1) * esz));
+        CU(S.flags.ensure((size_t)std::max<int64_t>(flag_total, 1) * sizeof(int)));
+        CU(cudaMemsetAsync(S.flags.p, 0, (size_t)std::max<int64_t>(flag_total, 1) * sizeof(int), S.st));
+        CU(S.h_passes.ensure(P.size() * sizeof(PassDesc)));
+        memcpy(S.h_passes.p, P.data(), P.size() * sizeof(PassDesc));
+        CU(S.passes.ensure(P.size() * sizeof(PassDesc)));
+        CU(S.counter.ensure(sizeof(int)));
+        CU(S.bnd.ensure((size_t)bnd_total * 8));
+        CU(cudaMemcpyAsync(S.passes.p, S.h_passes.p, P.size() * sizeof(PassDesc), cudaMemcpyHostToDevice, S.st));
         int64_t nitems = 0;
-        TRY(upload_queue(P, nitems));
-        CU(cudaMemsetAsync(c.counter.p, 0, sizeof(int), c.st));
-        CU(cudaMemsetAsync(c.bnd.p, 0xFF, (size_t)bnd_total * 8, c.st));  // tag -1
+        TRY(upload_queue(S, P, nitems));
+        CU(cudaMemsetAsync(S.counter.p, 0, sizeof(int), S.st));
+        CU(cudaMemsetAsync(S.bnd.p, 0xFF, (size_t)bnd_total * 8, S.st));  // tag -1
         WaveLaunch w{};
         w.X = c.xp.p;
         w.Y = c.yp.p;
         w.dp = dp;
         w.wide = dpl.wide;
         w.precision = prec;
-        w.passes = c.passes.as<PassDesc>();
-        w.items = c.items.as<WorkItem>();
+        w.passes = S.passes.as<PassDesc>();
+        w.items = S.items.as<WorkItem>();
         w.nitems = (int)nitems;
-        w.counter = c.counter.as<int>();
-        w.out = c.out.p;
-        w.bnd = c.bnd.p;
+        w.counter = S.counter.as<int>();
+        w.out = S.out.p;
+        w.bnd = S.bnd.p;
         w.bp = c.bp.as<unsigned long long>();
-        w.lb = c.lb.p;
+        w.lb = S.lb.p;
         if (const char* d = getenv("LMDTW_PROBE")) w.dbg = atoi(d);  // LMDTW_PROBES builds only
         // Latency-bound level: the longest strip has more serial tiles than the
         // level has tiles per pipeline -> half the pipelines per SM, so the
@@ -536,7 +580,7 @@ struct Engine {
             w.active_np = (head > 2.0 * per_pipe && np >= 2) ? np / 2 : np;
             if (const char* a = getenv("LMDTW_ACTIVE_NP")) w.active_np = atoi(a);
         }
-        w.flags = c.flags.as<int>();
+        w.flags = S.flags.as<int>();
         w.tab = tab;
         w.leaf_cost = lcost;
         w.tie0 = tie[0];
@@ -547,9 +591,9 @@ struct Engine {
         // LMDTW_TRACE_FILE: append per-strip DP start/end timestamps (debug)
         const char* trace_file = getenv("LMDTW_TRACE_FILE");
         if (trace_file) {
-            CU(c.trace.ensure(nitems * 24));
-            CU(cudaMemsetAsync(c.trace.p, 0, nitems * 24, c.st));
-            w.trace = c.trace.as<unsigned long long>();
+            CU(S.trace.ensure(nitems * 24));
+            CU(cudaMemsetAsync(S.trace.p, 0, nitems * 24, S.st));
+            w.trace = S.trace.as<unsigned long long>();
         }
         const bool prof = g_profile.load() != 0;
         if (getenv("LMDTW_HOST_TIMING"))
@@ -559,25 +603,25 @@ struct Engine {
         if (prof) {
             CU(c.prof_event(&pe0));
             CU(c.prof_event(&pe1));
-            CU(cudaEventRecord(c.evpool[pe0], c.st));
+            CU(cudaEventRecord(c.evpool[pe0], S.st));
         }
         if (getenv("LMDTW_HOST_TIMING")) {  // device-idle gap since the last sync point
             cudaEvent_t ev;
             cudaEventCreate(&ev);
-            cudaEventRecord(ev, c.st);
+            cudaEventRecord(ev, S.st);
             cudaEventSynchronize(ev);
             float ms = 0;
             if (g_last_sync_ev) cudaEventElapsedTime(&ms, g_last_sync_ev, ev);
             fprintf(stderr, "lmdtw host: device idle %.1f us before this wave launch\n", 1e3 * ms);
             cudaEventDestroy(ev);
         }
-        TRY(launched(launch_wave(w, c.st), leaf ? "leaf wave_kernel" : "wave_kernel"));
+        TRY(launched(launch_wave(w, S.st), leaf ? "leaf wave_kernel" : "wave_kernel"));
         if (trace_file) {
             std::vector<unsigned long long> tr(nitems * 3);
             std::vector<WorkItem> items(nitems);
-            CU(cudaMemcpyAsync(tr.data(), c.trace.p, tr.size() * 8, cudaMemcpyDeviceToHost, c.st));
-            CU(cudaMemcpyAsync(items.data(), c.items.p, nitems * sizeof(WorkItem), cudaMemcpyDeviceToHost, c.st));
-            CU(cudaStreamSynchronize(c.st));
+            CU(cudaMemcpyAsync(tr.data(), S.trace.p, tr.size() * 8, cudaMemcpyDeviceToHost, S.st));
+            CU(cudaMemcpyAsync(items.data(), S.items.p, nitems * sizeof(WorkItem), cudaMemcpyDeviceToHost, S.st));
+            CU(cudaStreamSynchronize(S.st));
             if (FILE* f = fopen(trace_file, "ab")) {
                 const long long hdr[3] = {(long long)P.size(), (long long)items.size(), (long long)leaf};
                 fwrite(hdr, sizeof hdr, 1, f);
@@ -588,7 +632,7 @@ struct Engine {
             }
         }
         if (prof) {
-            CU(cudaEventRecord(c.evpool[pe1], c.st));
+            CU(cudaEventRecord(c.evpool[pe1], S.st));
             c.pend.push_back(Ctx::Pend{pe0, pe1, (long long)cells, leaf});
         }
         return LMDTW_OK;
@@ -627,9 +671,12 @@ struct Engine {
     }
 
     // Batched find_pivot over `nodes` (indices into `all`).
-    int pivot_level(std::vector<Node>& all, const std::vector<int>& nodes, const std::vector<int64_t>& xb,
-                    const std::vector<int64_t>& yb, std::vector<int64_t>* cells_out,
-                    std::vector<int64_t>* peak_out, int highest) {
+    // pivot_launch: everything for one batch on slot S's stream, ending with
+    // the pivots' device->host copy and S.done; pivot_collect reads them back
+    // once S.done has completed.
+    int pivot_launch(Slot& S, std::vector<Node>& all, const std::vector<int>& nodes, const std::vector<int64_t>& xb,
+                     const std::vector<int64_t>& yb, std::vector<int64_t>* cells_out,
+                     std::vector<int64_t>* peak_out, int highest) {
         std::vector<PassDesc> P;
         std::vector<PivotDesc> V;
         int64_t out_total = 0, bnd_total = 0, cells = 0;
@@ -658,33 +705,27 @@ struct Engine {
             if (peak_out)
                 peak_out->push_back(std::max(peak_values(kf, n.M, n.N), peak_values(kb, n.M, n.N)));
         }
-        CU(c.out.ensure((size_t)out_total * esz));
-        TRY(run_wave(P, bnd_total, false, nullptr, nullptr, cells));
-        CU(c.pdesc.ensure(V.size() * sizeof(PivotDesc)));
-        CU(c.pout.ensure(V.size() * sizeof(PivotOut)));
-        CU(c.h_pdesc.ensure(V.size() * sizeof(PivotDesc)));
-        CU(c.h_pout.ensure(V.size() * sizeof(PivotOut)));
-        memcpy(c.h_pdesc.p, V.data(), V.size() * sizeof(PivotDesc));
-        CU(cudaMemcpyAsync(c.pdesc.p, c.h_pdesc.p, V.size() * sizeof(PivotDesc), cudaMemcpyHostToDevice, c.st));
+        CU(S.out.ensure((size_t)out_total * esz));
+        TRY(run_wave(S, P, bnd_total, false, nullptr, nullptr, cells));
+        CU(S.pdesc.ensure(V.size() * sizeof(PivotDesc)));
+        CU(S.pout.ensure(V.size() * sizeof(PivotOut)));
+        CU(S.h_pdesc.ensure(V.size() * sizeof(PivotDesc)));
+        CU(S.h_pout.ensure(V.size() * sizeof(PivotOut)));
+        memcpy(S.h_pdesc.p, V.data(), V.size() * sizeof(PivotDesc));
+        CU(cudaMemcpyAsync(S.pdesc.p, S.h_pdesc.p, V.size() * sizeof(PivotDesc), cudaMemcpyHostToDevice, S.st));
         const size_t scb = pivot_scratch_bytes((int)V.size());
-        CU(c.pscratch.ensure(scb));
-        CU(cudaMemsetAsync(c.pscratch.p, 0, scb, c.st));  // zeroes the per-node done counters
-        TRY(launched(launch_pivots(prec, c.passes.as<PassDesc>(), c.pdesc.as<PivotDesc>(), (int)V.size(), c.out.p,
-                                   c.pout.as<PivotOut>(), c.pscratch.p, c.st),
+        CU(S.pscratch.ensure(scb));
+        CU(cudaMemsetAsync(S.pscratch.p, 0, scb, S.st));  // zeroes the per-node done counters
+        TRY(launched(launch_pivots(prec, S.passes.as<PassDesc>(), S.pdesc.as<PivotDesc>(), (int)V.size(), S.out.p,
+                                   S.pout.as<PivotOut>(), S.pscratch.p, S.st),
                      "pivot_kernel"));
-        CU(cudaMemcpyAsync(c.h_pout.p, c.pout.p, V.size() * sizeof(PivotOut), cudaMemcpyDeviceToHost, c.st));
+        CU(cudaMemcpyAsync(S.h_pout.p, S.pout.p, V.size() * sizeof(PivotOut), cudaMemcpyDeviceToHost, S.st));
         c.d2h += V.size() * sizeof(PivotOut);
-        const auto ts0 = std::chrono::steady_clock::now();
-        CU(cudaStreamSynchronize(c.st));
-        c.prof_collect();
-        if (getenv("LMDTW_HOST_TIMING")) {
-            if (!g_last_sync_ev) cudaEventCreate(&g_last_sync_ev);
-            cudaEventRecord(g_last_sync_ev, c.st);
-        }
-        if (getenv("LMDTW_HOST_TIMING"))
-            fprintf(stderr, "lmdtw host: level waited %.1f us for the device\n",
-                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts0).count());
-        const PivotOut* po = c.h_pout.as<PivotOut>();
+        CU(cudaEventRecord(S.done, S.st));
+        return LMDTW_OK;
+    }
+    void pivot_collect(Slot& S, std::vector<Node>& all, const std::vector<int>& nodes) {
+        const PivotOut* po = S.h_pout.as<PivotOut>();
         for (size_t q = 0; q < nodes.size(); q++) {
             Node& n = all[nodes[q]];
             n.pi = po[q].i;
@@ -692,6 +733,14 @@ struct Engine {
             n.k = po[q].k;
             n.total = po[q].total;
         }
+    }
+    // Synchronous batch (single-level entry points).
+    int pivot_level(Slot& S, std::vector<Node>& all, const std::vector<int>& nodes, const std::vector<int64_t>& xb,
+                    const std::vector<int64_t>& yb, std::vector<int64_t>* cells_out,
+                    std::vector<int64_t>* peak_out, int highest) {
+        TRY(pivot_launch(S, all, nodes, xb, yb, cells_out, peak_out, highest));
+        CU(cudaEventSynchronize(S.done));
+        pivot_collect(S, all, nodes);
         return LMDTW_OK;
     }
 
@@ -749,7 +798,7 @@ struct Engine {
             CU(c.tab.ensure((size_t)all[leafs[0]].M * all[leafs[0]].N * esz));
             tab_dev = c.tab.p;
         }
-        TRY(run_wave(P, bnd_total, true, tab_dev, c.lcost.p, cells));
+        TRY(run_wave(c.main, P, bnd_total, true, tab_dev, c.lcost.p, cells));
         CU(c.ldesc.ensure(n * sizeof(LeafDesc)));
         CU(cudaMemcpyAsync(c.ldesc.p, L.data(), n * sizeof(LeafDesc), cudaMemcpyHostToDevice, c.st));
         CU(c.path.ensure((size_t)path_total * 2 * sizeof(int)));
@@ -860,50 +909,153 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
         nodes.push_back(n);
         level.push_back((int)nodes.size() - 1);
     }
-    std::vector<int> leafs;
+    // Dataflow over the recursion (replaces the level-synchronous loop): the
+    // internal nodes whose sub-blocks are known form batches; a batch is one
+    // wave launch (both half passes of each node) + one pivot launch + one
+    // small D2H copy on its own stream and buffers (a Slot), so up to
+    // kMaxFlights batches run concurrently -- a node's children start as soon
+    // as its own batch has finished, while slower nodes of its level still
+    // run; persistent CTAs of a draining batch exit and free SMs for the next.
+    // Results never depend on the schedule (every node is the same
+    // find_pivot call); the trace and path are rebuilt from the tree below.
+    std::vector<int> leafs, ready;
     int64_t nlevels = 0;
-    while (!level.empty()) {
-        std::vector<int> internal;
-        for (int q : level) {
-            const Node& n = nodes[q];
-            if (n.M < cfg.min_dim || n.N < cfg.min_dim || n.M + n.N <= 5) {
-                nodes[q].leaf = (int)leafs.size();
-                leafs.push_back(q);
-            } else {
-                internal.push_back(q);
+    auto classify = [&](int q) {
+        const Node& n = nodes[q];
+        if (n.M < cfg.min_dim || n.N < cfg.min_dim || n.M + n.N <= 5) {
+            nodes[q].leaf = (int)leafs.size();
+            leafs.push_back(q);
+        } else {
+            ready.push_back(q);
+            nlevels = std::max<int64_t>(nlevels, n.depth + 1);
+        }
+    };
+    for (int q : level) classify(q);
+    static const int kMaxFlights = [] {
+        const char* e = getenv("LMDTW_MAX_FLIGHTS");
+        const int v = e ? atoi(e) : 8;
+        return v < 1 ? 1 : (v > 32 ? 32 : v);
+    }();
+    cudaEvent_t staged;
+    CU(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
+    CU(cudaEventRecord(staged, c->st));  // features padded and cast
+    struct Flight {
+        Slot* S;
+        std::vector<int> ids;
+        std::vector<int64_t> cells, peaks;
+    };
+    std::vector<Flight> flights;
+    std::vector<Slot*> free_slots;
+    auto slot_for = [&](size_t k) -> Slot* {
+        if (k == 0) return &c->main;
+        while (c->extra.size() < k) {
+            std::unique_ptr<Slot> s(new Slot());
+            if (cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming) != cudaSuccess)
+                return nullptr;
+            c->extra.push_back(std::move(s));
+        }
+        return c->extra[k - 1].get();
+    };
+    for (int k = kMaxFlights - 1; k >= 0; k--) {
+        Slot* s = slot_for(k);
+        if (!s) {
+            cudaEventDestroy(staged);
+            return cuda_err(cudaGetLastError(), "batch stream");
+        }
+        free_slots.push_back(s);
+    }
+    int rc = LMDTW_OK;
+    while (rc == LMDTW_OK && (!ready.empty() || !flights.empty())) {
+        if (!ready.empty() && !free_slots.empty()) {
+            // split the ready nodes over the free slots, longest first (LPT by
+            // cells), but never into batches of fewer than ~1/8 of the ready
+            // work when many nodes are ready (launch count stays per level)
+            std::vector<int> order(ready);
+            std::sort(order.begin(), order.end(), [&](int a, int b) {
+                const int64_t ca = nodes[a].M * nodes[a].N, cb = nodes[b].M * nodes[b].N;
+                return ca != cb ? ca > cb : a < b;
+            });
+            const size_t nb = std::min(free_slots.size(), order.size());
+            std::vector<std::vector<int>> groups(nb);
+            std::vector<int64_t> load(nb, 0);
+            for (int q : order) {
+                size_t g = 0;
+                for (size_t k = 1; k < nb; k++)
+                    if (load[k] < load[g]) g = k;
+                groups[g].push_back(q);
+                load[g] += nodes[q].M * nodes[q].N;
+            }
+            ready.clear();
+            for (auto& g : groups) {
+                if (g.empty()) continue;
+                Flight f;
+                f.S = free_slots.back();
+                free_slots.pop_back();
+                std::sort(g.begin(), g.end());
+                f.ids = g;
+                if (cudaStreamWaitEvent(f.S->st, staged, 0) != cudaSuccess) {
+                    rc = cuda_err(cudaGetLastError(), "cudaStreamWaitEvent");
+                    break;
+                }
+                rc = E.pivot_launch(*f.S, nodes, f.ids, xb, yb, &f.cells, &f.peaks, cfg.pivot_highest);
+                if (rc != LMDTW_OK) break;
+                flights.push_back(std::move(f));
+            }
+            continue;
+        }
+        // a finished batch: the first whose event completed, else wait for the oldest
+        size_t k = flights.size();
+        for (size_t q = 0; q < flights.size() && k == flights.size(); q++) {
+            const cudaError_t e = cudaEventQuery(flights[q].S->done);
+            if (e == cudaSuccess) k = q;
+            else if (e != cudaErrorNotReady) rc = cuda_err(e, "batch");
+        }
+        if (rc != LMDTW_OK) break;
+        if (k == flights.size()) {
+            k = 0;
+            const cudaError_t e = cudaEventSynchronize(flights[0].S->done);
+            if (e != cudaSuccess) {
+                rc = cuda_err(e, "batch");
+                break;
             }
         }
-        if (internal.empty()) break;
-        nlevels++;
-        std::vector<int64_t> cells, peaks;
-        TRY(E.pivot_level(nodes, internal, xb, yb, &cells, &peaks, cfg.pivot_highest));
-        std::vector<int> next;
-        for (size_t q = 0; q < internal.size(); q++) {
-            const int id = internal[q];
+        Flight f = std::move(flights[k]);
+        flights.erase(flights.begin() + k);
+        E.pivot_collect(*f.S, nodes, f.ids);
+        free_slots.push_back(f.S);
+        for (size_t q = 0; q < f.ids.size(); q++) {
+            const int id = f.ids[q];
             Node parent = nodes[id];
             Inst& in = inst[parent.pair];
-            in.peak_diag = std::max(in.peak_diag, peaks[q]);
-            in.add_batch(cells[q]);
+            in.peak_diag = std::max(in.peak_diag, f.peaks[q]);
+            in.add_batch(f.cells[q]);
             Node l, r;
             l.i_off = parent.i_off;
             l.j_off = parent.j_off;
             l.M = parent.pi + 1;
             l.N = parent.pj + 1;
             l.pair = parent.pair;
+            l.depth = parent.depth + 1;
             r.i_off = parent.i_off + parent.pi;
             r.j_off = parent.j_off + parent.pj;
             r.M = parent.M - parent.pi;
             r.N = parent.N - parent.pj;
             r.pair = parent.pair;
+            r.depth = parent.depth + 1;
             nodes.push_back(l);
             nodes[id].left = (int)nodes.size() - 1;
-            next.push_back(nodes[id].left);
+            classify(nodes[id].left);
             nodes.push_back(r);
             nodes[id].right = (int)nodes.size() - 1;
-            next.push_back(nodes[id].right);
+            classify(nodes[id].right);
         }
-        level.swap(next);
     }
+    // on error: drain what is in flight before the buffers are reused
+    for (auto& f : flights) cudaEventSynchronize(f.S->done);
+    cudaEventDestroy(staged);
+    if (rc != LMDTW_OK) return rc;
+    c->prof_collect();
     // leaves, in node order (the stitching below walks the tree)
     std::vector<int64_t> poff;
     std::vector<int> plen;
@@ -1122,17 +1274,17 @@ int lmdtw_debug_wave_independent(int device, int32_t precision, int32_t d, int32
     std::vector<PassDesc> P;
     for (int q = 0; q < npasses; q++)
         P.push_back(E.half_pass_desc(xb[0], yb[0], M, N, M + N - 2, 0, out_total, bnd_total));
-    CU(c->out.ensure((size_t)out_total * E.esz));
+    CU(c->main.out.ensure((size_t)out_total * E.esz));
     double tot = 0;
     for (int r = 0; r < reps + 1; r++) {
-        TRY(E.run_wave(P, bnd_total, false, nullptr, nullptr, 0));
+        TRY(E.run_wave(c->main, P, bnd_total, false, nullptr, nullptr, 0));
         CU(cudaEventRecord(c->ev1, c->st));
         CU(cudaEventSynchronize(c->ev1));
         if (r == 0) continue;  // warm-up
     }
     // time the last `reps` launches as one block
     CU(cudaEventRecord(c->ev0, c->st));
-    for (int r = 0; r < reps; r++) TRY(E.run_wave(P, bnd_total, false, nullptr, nullptr, 0));
+    for (int r = 0; r < reps; r++) TRY(E.run_wave(c->main, P, bnd_total, false, nullptr, nullptr, 0));
     CU(cudaEventRecord(c->ev1, c->st));
     CU(cudaEventSynchronize(c->ev1));
     float f = 0;
@@ -1177,32 +1329,32 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     pd.bnd_off = 0;
     pd.bnd_in_first = strip_lo > 0 ? (uint64_t)(uintptr_t)bnd_prev : 0;
     pd.sys_out = strip_hi < pd.nstrips ? 1 : 0;  // the next shard may run on a peer GPU
-    CU(c->out.ensure((size_t)out_total * E.esz));
-    CU(c->passes.ensure(sizeof(PassDesc)));
-    CU(c->counter.ensure(sizeof(int)));
-    CU(c->lb.ensure((size_t)pd.nstrips * (H + 1) * E.esz));
-    CU(c->flags.ensure((size_t)pd.nstrips * sizeof(int)));
-    CU(c->h_passes.ensure(sizeof(PassDesc)));
-    memcpy(c->h_passes.p, &pd, sizeof(PassDesc));
-    CU(cudaMemcpyAsync(c->passes.p, c->h_passes.p, sizeof(PassDesc), cudaMemcpyHostToDevice, c->st));
+    CU(c->main.out.ensure((size_t)out_total * E.esz));
+    CU(c->main.passes.ensure(sizeof(PassDesc)));
+    CU(c->main.counter.ensure(sizeof(int)));
+    CU(c->main.lb.ensure((size_t)pd.nstrips * (H + 1) * E.esz));
+    CU(c->main.flags.ensure((size_t)pd.nstrips * sizeof(int)));
+    CU(c->main.h_passes.ensure(sizeof(PassDesc)));
+    memcpy(c->main.h_passes.p, &pd, sizeof(PassDesc));
+    CU(cudaMemcpyAsync(c->main.passes.p, c->main.h_passes.p, sizeof(PassDesc), cudaMemcpyHostToDevice, c->st));
     int64_t nitems = 0;
-    TRY(E.upload_queue(std::vector<PassDesc>{pd}, nitems));
-    CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
-    CU(cudaMemsetAsync(c->flags.p, 0, (size_t)pd.nstrips * sizeof(int), c->st));
+    TRY(E.upload_queue(c->main, std::vector<PassDesc>{pd}, nitems));
+    CU(cudaMemsetAsync(c->main.counter.p, 0, sizeof(int), c->st));
+    CU(cudaMemsetAsync(c->main.flags.p, 0, (size_t)pd.nstrips * sizeof(int), c->st));
     WaveLaunch w{};
     w.X = c->xp.p;
     w.Y = c->yp.p;
     w.dp = E.dp;
     w.wide = E.dpl.wide;
     w.precision = precision;
-    w.passes = c->passes.as<PassDesc>();
-    w.items = c->items.as<WorkItem>();
+    w.passes = c->main.passes.as<PassDesc>();
+    w.items = c->main.items.as<WorkItem>();
     w.nitems = (int)nitems;
-    w.counter = c->counter.as<int>();
-    w.out = c->out.p;
+    w.counter = c->main.counter.as<int>();
+    w.out = c->main.out.p;
     w.bnd = bnd_local;
-    w.lb = c->lb.p;
-    w.flags = c->flags.as<int>();
+    w.lb = c->main.lb.p;
+    w.flags = c->main.flags.as<int>();
     w.tie0 = 2;
     w.tie1 = 0;
     w.tie2 = 1;
@@ -1217,10 +1369,10 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
         if (r1 < r0) continue;
         const int64_t i0 = top - r1, cnt = r1 - r0 + 1;
         if (out_d && out_d[s3])
-            CU(cudaMemcpyAsync((char*)out_d[s3] + i0 * E.esz, (char*)c->out.p + (pd.out_off[s3] + i0) * E.esz,
+            CU(cudaMemcpyAsync((char*)out_d[s3] + i0 * E.esz, (char*)c->main.out.p + (pd.out_off[s3] + i0) * E.esz,
                                cnt * E.esz, cudaMemcpyDefault, c->st));
         if (out_c && out_c[s3])
-            CU(cudaMemcpyAsync((char*)out_c[s3] + i0 * E.esz, (char*)c->out.p + (pd.out_off[3 + s3] + i0) * E.esz,
+            CU(cudaMemcpyAsync((char*)out_c[s3] + i0 * E.esz, (char*)c->main.out.p + (pd.out_off[3 + s3] + i0) * E.esz,
                                cnt * E.esz, cudaMemcpyDefault, c->st));
     }
     CU(cudaStreamSynchronize(c->st));
@@ -1326,7 +1478,7 @@ int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const f
         z.pd.tile_w = kTileW;
         z.pd.lb_off = 0;
         z.pd.flag_off = 0;
-        E.make_items(std::vector<PassDesc>{z.pd}, z.items);
+        E.make_items(c->main, std::vector<PassDesc>{z.pd}, z.items);
         if (z.bnd.ensure((size_t)bnd_total * 8) != cudaSuccess || z.out.ensure((size_t)out_total * E.esz) ||
             z.passes.ensure(sizeof(PassDesc)) || z.items_d.ensure(z.items.size() * sizeof(WorkItem)) ||
             z.counter.ensure(sizeof(int)) || z.lb.ensure((size_t)S * (H + 1) * E.esz) ||
@@ -1412,16 +1564,16 @@ int lmdtw_half_pass(int device, const float* X, int64_t M, const float* Y, int64
     TRY(E.stage(&Y, &N, 1, mem, false, yb));
     int64_t out_total = 0, bnd_total = 0;
     std::vector<PassDesc> P{E.half_pass_desc(xb[0], yb[0], M, N, kstop, reverse ? 1 : 0, out_total, bnd_total)};
-    CU(c->out.ensure((size_t)out_total * E.esz));
+    CU(c->main.out.ensure((size_t)out_total * E.esz));
     const int64_t cl = cells_upto(kstop, M, N);
-    TRY(E.run_wave(P, bnd_total, false, nullptr, nullptr, cl));
+    TRY(E.run_wave(c->main, P, bnd_total, false, nullptr, nullptr, cl));
     for (int s = 0; s < 3; s++) {
         const int64_t L = dlen(kstop - 2 + s, M, N);
         if (L > 0 && out_d && out_d[s])
-            CU(cudaMemcpyAsync(out_d[s], (char*)c->out.p + P[0].out_off[s] * E.esz, L * E.esz,
+            CU(cudaMemcpyAsync(out_d[s], (char*)c->main.out.p + P[0].out_off[s] * E.esz, L * E.esz,
                                cudaMemcpyDefault, c->st));
         if (L > 0 && out_c && out_c[s])
-            CU(cudaMemcpyAsync(out_c[s], (char*)c->out.p + P[0].out_off[3 + s] * E.esz, L * E.esz,
+            CU(cudaMemcpyAsync(out_c[s], (char*)c->main.out.p + P[0].out_off[3 + s] * E.esz, L * E.esz,
                                cudaMemcpyDefault, c->st));
     }
     CU(cudaStreamSynchronize(c->st));
@@ -1450,7 +1602,7 @@ int lmdtw_find_pivot(int device, const float* X, int64_t M, const float* Y, int6
     nodes[0].N = N;
     nodes[0].pair = 0;
     std::vector<int64_t> cl, pk;
-    TRY(E.pivot_level(nodes, std::vector<int>{0}, xb, yb, &cl, &pk, pivot_highest ? 1 : 0));
+    TRY(E.pivot_level(c->main, nodes, std::vector<int>{0}, xb, yb, &cl, &pk, pivot_highest ? 1 : 0));
     if (i) *i = nodes[0].pi;
     if (j) *j = nodes[0].pj;
     if (diagonal_k) *diagonal_k = nodes[0].k;
@@ -1547,7 +1699,7 @@ int lmdtw_pivot_nodes(int device, const float* X, int64_t M, const float* Y, int
         ids[q] = q;
     }
     std::vector<int64_t> cl, pk;
-    TRY(E.pivot_level(nodes, ids, xb, yb, &cl, &pk, pivot_highest ? 1 : 0));
+    TRY(E.pivot_level(c->main, nodes, ids, xb, yb, &cl, &pk, pivot_highest ? 1 : 0));
     for (int q = 0; q < n; q++) {
         out[5 * q] = nodes[q].pi;
         out[5 * q + 1] = nodes[q].pj;
@@ -1652,16 +1804,16 @@ int lmdtw_pivot_combine_device(int device, int32_t precision, int64_t M, int64_t
         P[1].out_off[s] = off;
         off += dlen(kb - 2 + s, M, N);
     }
-    CU(c->out.ensure((size_t)std::max<int64_t>(off, 1) * esz));
+    CU(c->main.out.ensure((size_t)std::max<int64_t>(off, 1) * esz));
     for (int s = 0; s < 3; s++) {
         const int64_t Lf = dlen(kf - 2 + s, M, N), Lb = dlen(kb - 2 + s, M, N);
         if (Lf > 0) {
-            CU(cudaMemcpyAsync((char*)c->out.p + P[0].out_off[s] * esz, fwd_d[s], Lf * esz, cudaMemcpyDefault, c->st));
-            CU(cudaMemcpyAsync((char*)c->out.p + P[0].out_off[3 + s] * esz, fwd_c[s], Lf * esz, cudaMemcpyDefault,
+            CU(cudaMemcpyAsync((char*)c->main.out.p + P[0].out_off[s] * esz, fwd_d[s], Lf * esz, cudaMemcpyDefault, c->st));
+            CU(cudaMemcpyAsync((char*)c->main.out.p + P[0].out_off[3 + s] * esz, fwd_c[s], Lf * esz, cudaMemcpyDefault,
                                c->st));
         }
         if (Lb > 0)
-            CU(cudaMemcpyAsync((char*)c->out.p + P[1].out_off[s] * esz, bwd_d[s], Lb * esz, cudaMemcpyDefault, c->st));
+            CU(cudaMemcpyAsync((char*)c->main.out.p + P[1].out_off[s] * esz, bwd_d[s], Lb * esz, cudaMemcpyDefault, c->st));
     }
     PivotDesc v{};
     v.fwd = 0;
@@ -1671,19 +1823,19 @@ int lmdtw_pivot_combine_device(int device, int32_t precision, int64_t M, int64_t
     v.kf = (int32_t)kf;
     v.kb = (int32_t)kb;
     v.highest = pivot_highest ? 1 : 0;
-    CU(c->passes.ensure(sizeof P));
-    CU(c->pdesc.ensure(sizeof v));
-    CU(c->pout.ensure(sizeof(PivotOut)));
-    CU(cudaMemcpyAsync(c->passes.p, P, sizeof P, cudaMemcpyHostToDevice, c->st));
-    CU(cudaMemcpyAsync(c->pdesc.p, &v, sizeof v, cudaMemcpyHostToDevice, c->st));
+    CU(c->main.passes.ensure(sizeof P));
+    CU(c->main.pdesc.ensure(sizeof v));
+    CU(c->main.pout.ensure(sizeof(PivotOut)));
+    CU(cudaMemcpyAsync(c->main.passes.p, P, sizeof P, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->main.pdesc.p, &v, sizeof v, cudaMemcpyHostToDevice, c->st));
     const size_t scb = pivot_scratch_bytes(1);
-    CU(c->pscratch.ensure(scb));
-    CU(cudaMemsetAsync(c->pscratch.p, 0, scb, c->st));
-    CU(launch_pivots(precision, c->passes.as<PassDesc>(), c->pdesc.as<PivotDesc>(), 1, c->out.p,
-                     c->pout.as<PivotOut>(), c->pscratch.p, c->st));
+    CU(c->main.pscratch.ensure(scb));
+    CU(cudaMemsetAsync(c->main.pscratch.p, 0, scb, c->st));
+    CU(launch_pivots(precision, c->main.passes.as<PassDesc>(), c->main.pdesc.as<PivotDesc>(), 1, c->main.out.p,
+                     c->main.pout.as<PivotOut>(), c->main.pscratch.p, c->st));
     g_launches++;
     PivotOut po{};
-    CU(cudaMemcpyAsync(&po, c->pout.p, sizeof po, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(&po, c->main.pout.p, sizeof po, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
     ijk[0] = po.i;
     ijk[1] = po.j;
