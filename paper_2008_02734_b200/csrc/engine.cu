@@ -385,7 +385,26 @@ struct Node {
 
 struct Engine {
     Ctx& c;
-    int prec, d, dp, H;  // dp: padded row length (elements)
+    int prec, d, dp, H;  // dp: padded row length (elements); H: strip height of the launch being built
+    int lat = 0;         // the launch being built uses the latency variant (strip_height(.., 1))
+    int lat_policy = 1;  // LMDTW_LAT: 0 never, 1 latency-bound launches, 2 always
+    void set_lat(int l) {
+        lat = (l && !dpl.wide) ? 1 : 0;
+        H = strip_height(prec, dpl, lat);
+    }
+    // A launch is latency-bound when its longest strip has more serial tiles
+    // than the launch has tiles per pipeline (twice over): the head strips'
+    // chain, not the FMA pipes, then sets the time.
+    bool latency_bound(const std::vector<PassDesc>& P) {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
+        int64_t head = 0, tiles = 0;
+        for (const auto& p : P) {
+            head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
+            for (int a = p.strip_lo; a < p.strip_hi; a++) tiles += tiles_of(p, a, H);
+        }
+        return head > 2.0 * (double)tiles / ((double)pipes_per_cta(prec, dpl, lat) * nsm);
+    }
     DimPlan dpl;
     size_t esz;
     int tie[3] = {2, 0, 1};
@@ -393,6 +412,8 @@ struct Engine {
         dpl = plan_dims(prec, d);
         dp = dpl.dp;
         H = strip_height(prec, dpl);
+        const char* e = getenv("LMDTW_LAT");  // 0: never use the latency variant, 2: always
+        lat_policy = e ? atoi(e) : 1;
         esz = prec == 32 ? 4 : 8;
     }
 
@@ -573,7 +594,7 @@ struct Engine {
         {
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
-            const int np = pipes_per_cta(prec, dpl);
+            const int np = pipes_per_cta(prec, dpl, lat);
             int64_t head = 0;
             for (const auto& p : P) head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
             const double per_pipe = (double)nitems / ((double)np * nsm);
@@ -588,6 +609,7 @@ struct Engine {
         w.tie2 = tie[2];
         w.leaf = leaf ? 1 : 0;
         w.grid_warps = 0;
+        w.lat = lat;
         // LMDTW_TRACE_FILE: append per-strip DP start/end timestamps (debug)
         const char* trace_file = getenv("LMDTW_TRACE_FILE");
         if (trace_file) {
@@ -680,6 +702,22 @@ struct Engine {
         std::vector<PassDesc> P;
         std::vector<PivotDesc> V;
         int64_t out_total = 0, bnd_total = 0, cells = 0;
+        // latency variant for latency-bound batches (decided on the default strips)
+        set_lat(0);
+        if (lat_policy == 2) {
+            set_lat(1);
+        } else if (lat_policy == 1) {
+            for (int q : nodes) {
+                const Node& n = all[q];
+                const int64_t K = n.M + n.N - 1, kf = (K + 1) / 2, kb = (K % 2 == 0) ? kf + 1 : kf;
+                P.push_back(half_pass_desc(0, 0, n.M, n.N, kf, 0, out_total, bnd_total));
+                P.push_back(half_pass_desc(0, 0, n.M, n.N, kb, 1, out_total, bnd_total));
+            }
+            const bool lb = latency_bound(P);
+            P.clear();
+            out_total = bnd_total = 0;
+            set_lat(lb ? 1 : 0);
+        }
         P.reserve(nodes.size() * 2);
         for (int q : nodes) {
             const Node& n = all[q];
@@ -750,6 +788,13 @@ struct Engine {
                const std::vector<int64_t>& yb, void* tab_host, std::vector<int64_t>& path_off,
                std::vector<int>& plen) {
         const int n = (int)leafs.size();
+        {
+            static const int leaf_lat = [] {
+                const char* e = getenv("LMDTW_LAT_LEAF");  // leaves in the latency variant
+                return e ? atoi(e) : 0;
+            }();
+            set_lat(leaf_lat);
+        }
         std::vector<PassDesc> P(n);
         std::vector<LeafDesc> L(n);
         int64_t bnd_total = 0, bp_total = 0, path_total = 0, cells = 0;
@@ -933,7 +978,10 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     for (int q : level) classify(q);
     static const int kMaxFlights = [] {
         const char* e = getenv("LMDTW_MAX_FLIGHTS");
-        const int v = e ? atoi(e) : 8;
+        // 1: one batch per recursion level (default: concurrent persistent
+        // grids serialise -- the first holds every SM while its wavefront
+        // ramps, measured 36 -> 52 ms at cfg3 with 8 slots)
+        const int v = e ? atoi(e) : 1;
         return v < 1 ? 1 : (v > 32 ? 32 : v);
     }();
     cudaEvent_t staged;

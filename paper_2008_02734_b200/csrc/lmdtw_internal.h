@@ -106,6 +106,7 @@ struct WaveLaunch {
     int active_np;          // pipelines per CTA taking work (0 = all)
     int grid_warps;         // persistent warps to launch (0 = auto)
     unsigned long long* trace;  // optional per-item timestamps (debug)
+    int lat;                // 1: latency variant (strip height strip_height(.., 1))
 };
 
 // How feature rows of dimension d are laid out and which kernels run them:
@@ -118,8 +119,10 @@ struct DimPlan {
 };
 constexpr int kMaxDim = 1 << 16;
 DimPlan plan_dims(int precision, int d);
-int strip_height(int precision, DimPlan dp);  // grid rows per strip
-int pipes_per_cta(int precision, DimPlan dp);
+// lat = 1: the latency variant (half the rows per lane) for levels whose
+// head strips are on the critical path
+int strip_height(int precision, DimPlan dp, int lat = 0);  // grid rows per strip
+int pipes_per_cta(int precision, DimPlan dp, int lat = 0);
 cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
 // Tile queue: tile b of entry e goes to slot cursor[b*key_per_tile + strip]++
 // (cursor = first slot of each key, consumed).
@@ -134,7 +137,7 @@ cudaError_t launch_backtrace(int precision, DimPlan dp, const void* X, const voi
                              int* plen, cudaStream_t stream);
 cudaError_t launch_pad_cast(int precision, const float* src, int64_t rows, int d, int dp, void* dst,
                             cudaStream_t stream);
-int max_resident_warps(int precision, DimPlan dp, int leaf, int device);
+int max_resident_warps(int precision, DimPlan dp, int leaf, int device, int lat = 0);
 
 // ---- window.cu: windowed DP (approx._window_fill), path costs, discrepancy
 // One constrained_dtw problem: rows [0, M) of a monotone staircase window
