@@ -88,6 +88,11 @@ CONFIGS = {
     "cfg4": dict(workload="256 pairs M,N~U[5k,30k] d=12 chroma-like (rng 4)", batch=256, d=12, prec=32),
     "cfg5": dict(workload="M=200000 N=20000 d=48 latent walk seed 5 (fp64)", M=200000, N=20000, d=48, seed=5,
                  prec=64),
+    # the reference extractor's feature width (mfcc-mod / DLNC0, d = 100): the WIDE kernels
+    "d100": dict(workload="latent walk M=N=20000 d=100 seed 100 (fp32)", M=20000, N=20000, d=100, seed=100,
+                 prec=32),
+    "d100x64": dict(workload="latent walk M=N=20000 d=100 seed 100 (fp64)", M=20000, N=20000, d=100, seed=100,
+                    prec=64),
 }
 
 
@@ -105,7 +110,7 @@ def make_inputs(name):
         rng = np.random.default_rng(4)
         MN = rng.integers(5000, 30001, size=(c["batch"], 2))
         return [chroma_pair(int(m), int(n), 12, seed=1000 + q) for q, (m, n) in enumerate(MN)]
-    if name == "cfg5":
+    if name in ("cfg5", "d100", "d100x64"):
         return [latent_pair(c["M"], c["N"], c["d"], c["seed"])]
     return [chroma_pair(c["M"], c["N"], c["d"], c["seed"])]
 

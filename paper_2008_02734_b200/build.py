@@ -39,12 +39,16 @@ def _stale(target, deps):
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     objs, procs = [], []
-    for src in SOURCES:
+    # kernels.cu is compiled twice (fp32 / fp64 strip engines) so the two
+    # halves build in parallel
+    units = [("kernels.cu", "kernels_f32.o", ["-DLMDTW_TU=32"]), ("kernels.cu", "kernels_f64.o", ["-DLMDTW_TU=64"])]
+    units += [(src, src.replace(".cu", ".o"), []) for src in SOURCES if src != "kernels.cu"]
+    for src, obj, defs in units:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        o = os.path.join(OBJDIR, obj)
         objs.append(o)
         if force or _stale(o, [s] + HEADERS):
-            cmd = [NVCC] + ARCH + FLAGS + ["-c", s, "-o", o]
+            cmd = [NVCC] + ARCH + FLAGS + defs + ["-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), flush=True)
             procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

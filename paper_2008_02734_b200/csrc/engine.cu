@@ -389,7 +389,8 @@ struct Engine {
     int lat = 0;         // the launch being built uses the latency variant (strip_height(.., 1))
     int lat_policy = 1;  // LMDTW_LAT: 0 never, 1 latency-bound launches, 2 always
     void set_lat(int l) {
-        lat = (l && !dpl.wide) ? 1 : 0;
+        (void)l;  // the latency variant is not dispatched (kernels.cu, WsCfg::R)
+        lat = 0;
         H = strip_height(prec, dpl, lat);
     }
     // A launch is latency-bound when its longest strip has more serial tiles
@@ -412,8 +413,7 @@ struct Engine {
         dpl = plan_dims(prec, d);
         dp = dpl.dp;
         H = strip_height(prec, dpl);
-        const char* e = getenv("LMDTW_LAT");  // 0: never use the latency variant, 2: always
-        lat_policy = e ? atoi(e) : 1;
+        lat_policy = 0;  // the latency variant is not dispatched (see WsCfg::R)
         esz = prec == 32 ? 4 : 8;
     }
 

@@ -124,6 +124,12 @@ DimPlan plan_dims(int precision, int d);
 int strip_height(int precision, DimPlan dp, int lat = 0);  // grid rows per strip
 int pipes_per_cta(int precision, DimPlan dp, int lat = 0);
 cudaError_t launch_wave(const WaveLaunch& w, cudaStream_t stream);
+// per-precision halves (kernels.cu compiled as two units, LMDTW_TU=32 / 64)
+cudaError_t launch_wave_f32(const WaveLaunch& w, cudaStream_t stream);
+cudaError_t launch_wave_f64(const WaveLaunch& w, cudaStream_t stream);
+int max_resident_warps_f32(DimPlan dp, int leaf, int device, int lat);
+int max_resident_warps_f64(DimPlan dp, int leaf, int device, int lat);
+cudaError_t set_watchdog_ns_f64(unsigned long long ns);
 // Tile queue: tile b of entry e goes to slot cursor[b*key_per_tile + strip]++
 // (cursor = first slot of each key, consumed).
 cudaError_t launch_scatter_items(const StripEnt* ents, int nents, int32_t* cursor, int key_per_tile,
