@@ -468,7 +468,15 @@ struct Engine {
     // predecessors of a tile come earlier in the queue -- the persistent
     // kernel's deadlock freedom -- and pipelines rotate over the strips
     // instead of holding a long strip while shorter ones wait behind it.
-    static constexpr int64_t kLagKey = 128;
+    // LMDTW_LAG_KEY (experiments): a divisor of kTileW; default 128
+    static int64_t lag_key() {
+        static const int64_t v = [] {
+            const char* e = getenv("LMDTW_LAG_KEY");
+            const int64_t k = e ? atoll(e) : 128;
+            return (k >= 16 && kTileW % k == 0) ? k : 128;
+        }();
+        return v;
+    }
     static int64_t tiles_of(const PassDesc& p, int a, int H) {
         const int64_t jend = std::min<int64_t>(p.N - 1, (int64_t)p.kstop - (int64_t)a * H);
         return jend / kTileW + 1;
@@ -480,8 +488,7 @@ struct Engine {
     // themselves are scattered on the device (scatter_items_kernel), so the
     // host never touches the O(tiles) queue.  Returns the number of tiles.
     int64_t stage_items(Slot& S, const std::vector<PassDesc>& P, int64_t& nents, int64_t& nkeys) {
-        static_assert(kTileW % kLagKey == 0, "tile width must be a multiple of the key lag");
-        constexpr int64_t kPer = kTileW / kLagKey;
+        const int64_t kPer = kTileW / lag_key();
         int64_t mmax = 0, total = 0;
         nents = 0;
         for (const auto& p : P) {
@@ -529,14 +536,14 @@ struct Engine {
         CU(cudaMemcpyAsync(S.istage.p, S.h_istage.p, stage_bytes, cudaMemcpyHostToDevice, S.st));
         return launched(launch_scatter_items(S.istage.as<StripEnt>(), (int)nents,
                                              reinterpret_cast<int32_t*>(S.istage.as<char>() + ent_bytes),
-                                             (int)(kTileW / kLagKey), S.items.as<WorkItem>(), S.st),
+                                             (int)(kTileW / lag_key()), S.items.as<WorkItem>(), S.st),
                         "scatter_items_kernel");
     }
 
     // Host-built queue (debug entry points only): same order as the device
     // scatter up to the order of tiles that share a key.
     void make_items(Slot& S, const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
-        constexpr int64_t kPer = kTileW / kLagKey;
+        const int64_t kPer = kTileW / lag_key();
         int64_t nents = 0, nkeys = 0;
         const int64_t total = stage_items(S, P, nents, nkeys);
         std::vector<int32_t> cur(S.h_istage.as<int32_t>() + nents * 3, S.h_istage.as<int32_t>() + nents * 3 + nkeys);
