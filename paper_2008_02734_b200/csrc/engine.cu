@@ -14,6 +14,7 @@
 // accumulation dtype (core.py:191-197).
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -942,6 +943,15 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     E.tie[1] = cfg.tie[1];
     E.tie[2] = cfg.tie[2];
     std::vector<int64_t> xb, yb;
+    // LMDTW_PHASES=1: host timestamps of the phases of this call (diagnostics)
+    const bool phases = getenv("LMDTW_PHASES") != nullptr;
+    const auto tp0 = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+        if (phases)
+            fprintf(stderr, "lmdtw phase %-18s %8.1f us\n", what,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tp0).count());
+    };
+    phase("leased");
     TRY(E.stage(X, M, npairs, mem, true, xb));
     TRY(E.stage(Y, N, npairs, mem, false, yb));
 
@@ -1053,7 +1063,9 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
                     rc = cuda_err(cudaGetLastError(), "cudaStreamWaitEvent");
                     break;
                 }
+                phase("batch launch");
                 rc = E.pivot_launch(*f.S, nodes, f.ids, xb, yb, &f.cells, &f.peaks, cfg.pivot_highest);
+                phase("batch launched");
                 if (rc != LMDTW_OK) break;
                 flights.push_back(std::move(f));
             }
@@ -1075,6 +1087,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
                 break;
             }
         }
+        phase("batch done");
         Flight f = std::move(flights[k]);
         flights.erase(flights.begin() + k);
         E.pivot_collect(*f.S, nodes, f.ids);
@@ -1114,10 +1127,16 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     // leaves, in node order (the stitching below walks the tree)
     std::vector<int64_t> poff;
     std::vector<int> plen;
+    phase("recursion done");
     TRY(E.leaves(nodes, leafs, xb, yb, nullptr, poff, plen));
+    phase("leaves done");
 
     const int* hpath = c->h_path.as<int>();
     results.assign(npairs, nullptr);
+    struct PhaseEnd {
+        std::function<void()> f;
+        ~PhaseEnd() { f(); }
+    } phase_end{[&] { phase("results built"); }};
     for (int p = 0; p < npairs; p++) {
         std::unique_ptr<lmdtw_result> res(new lmdtw_result());
         Inst& in = inst[p];

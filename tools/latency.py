@@ -40,6 +40,6 @@ for name in sys.argv[1:] or ["cfg1", "cfg2"]:
     dt = (time.perf_counter() - t) / reps
     print(f"{name}: {dt * 1e3:.3f} ms per alignment, {info.cells_processed / dt / 1e9:.1f} GCUPS, "
           f"{info.n_levels} levels, {info.gpu_launches} launches", flush=True)
-    os.environ["LMDTW_HOST_TIMING"] = "1"
+    os.environ["LMDTW_PHASES"] = "1"
     once()
-    del os.environ["LMDTW_HOST_TIMING"]
+    del os.environ["LMDTW_PHASES"]
