@@ -19,7 +19,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "liblmdtw_b200.so")
 OBJDIR = os.path.join(HERE, "_build")
 SOURCES = ["kernels.cu", "window.cu", "engine.cu"]
-HEADERS = [os.path.join(CSRC, "lmdtw_internal.h"), os.path.join(INCLUDE, "lmdtw_b200.h")]
+HEADERS = [os.path.join(CSRC, "lmdtw_internal.h"), os.path.join(CSRC, "sqrt64_fast.cuh"), os.path.join(INCLUDE, "lmdtw_b200.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
