@@ -38,7 +38,10 @@ struct PassDesc {
 // Columns per work item: a strip is cut into tiles of kTileW columns so the
 // persistent pipelines rotate over strips instead of holding one strip for
 // its whole length (a multiple of 32 and of the ring chunk).
-constexpr int kTileW = 2048;
+#ifndef LMDTW_TILE_W
+#define LMDTW_TILE_W 2048
+#endif
+constexpr int kTileW = LMDTW_TILE_W;
 
 // One tile: strip `strip` of pass `pass`, columns [blk * tile_w, ...).
 struct WorkItem {
