@@ -1,7 +1,7 @@
 """Leaf solvers on small full grids: the strip engine (dtw_full) vs the band
 kernel (constrained_dtw with a full window), wall time per call."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_2008_02734_b200 as L
 import bench

@@ -1,6 +1,6 @@
 // Issue/pipe throughput of the instruction forms the exact cost computation can
 // use (independent chains, W warps per SMSP), in warp-instructions per clock
-// per SMSP.  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/pipes tools/pipes.cu
+// per SMSP.  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/pipes tools/probes/pipes.cu
 #include <cstdio>
 typedef unsigned long long u64;
 

@@ -1,5 +1,5 @@
 """Small workloads for compute-sanitizer (racecheck / synccheck / memcheck):
-    compute-sanitizer --tool racecheck python tools/sanitize_case.py {align,shard}
+    compute-sanitizer --tool racecheck python tools/probes/sanitize_case.py {align,shard}
 align: linmdtw (half passes, pivots, leaves, backtrace) in fp32 and fp64;
 shard: one half pass cut into 3 concurrent strip shards whose first strips
 read the previous shard's handoff buffer (the multi-GPU handoff protocol)."""
@@ -7,7 +7,7 @@ import ctypes as C
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 

@@ -1,6 +1,6 @@
 """One cfg3 alignment with LMDTW_TRACE_FILE set (run on the GPU box)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import bench
 import paper_2008_02734_b200 as L
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"

@@ -1,6 +1,6 @@
 """Blocked-wait cycles per mbarrier tag for an independent-strip run (LMDTW_WAITSTATS build)."""
 import ctypes as C, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2008_02734_b200 import _capi
 lib = _capi.load()
 cyc = (C.c_ulonglong * 16)(); cnt = (C.c_ulonglong * 16)()

@@ -1,4 +1,6 @@
-"""Summarise gpurun_out/ evidence of tools/final_capture.sh into profiles/r1/final/."""
+"""Summarise gpurun_out/ evidence of tools/final_capture.sh into profiles/<round>/final/.
+
+    python tools/write_profiles.py [TAG] [ROUND]     (defaults: r1final r1)"""
 import csv
 import json
 import os
@@ -6,7 +8,9 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "profiles", "r1", "final")
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r1final"
+RND = sys.argv[2] if len(sys.argv) > 2 else "r1"
+OUT = os.path.join(ROOT, "profiles", RND, "final")
 G = os.path.join(ROOT, "gpurun_out")
 os.makedirs(OUT, exist_ok=True)
 
@@ -16,7 +20,7 @@ def last_json(path):
 
 
 # launch list of one bench step
-rows = [r for r in csv.reader(open(os.path.join(G, "launches_r1final.csv"))) if len(r) > 10 and r[0].isdigit()]
+rows = [r for r in csv.reader(open(os.path.join(G, f"launches_{TAG}.csv"))) if len(r) > 10 and r[0].isdigit()]
 step = []
 for r in rows:
     step.append((r[4].split("(")[0].replace("void ", ""), r[8], float(r[-1]) / 1e6))
@@ -34,8 +38,8 @@ with open(os.path.join(OUT, "launch_summary.txt"), "w") as f:
     f.write(f"  total {tot:.3f} ms\n")
     for n, t in sorted(agg.items(), key=lambda kv: -kv[1]):
         f.write(f"  share {100 * t / tot:5.1f}%  {n}\n")
-subprocess.run(["cp", os.path.join(G, "launches_r1final.csv"), os.path.join(OUT, "launches_cfg3.csv")])
-rep = os.path.join(G, "r1final.ncu-rep")
+subprocess.run(["cp", os.path.join(G, f"launches_{TAG}.csv"), os.path.join(OUT, "launches_cfg3.csv")])
+rep = os.path.join(G, f"{TAG}.ncu-rep")
 with open(os.path.join(OUT, "wave_kernel_level0_full.txt"), "w") as f:
     f.write(subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep, "20"],
                            capture_output=True, text=True).stdout)
@@ -59,12 +63,15 @@ rd, wr = metric("dram__bytes_read.sum"), metric("dram__bytes_write.sum")
 traffic = {"cfg3": {"launch": "wave_kernel<float,12,0> level 0 (1 node, fwd+rev half passes)",
                     "dram_bytes_read": int(rd), "dram_bytes_write": int(wr), "per_launch_bytes": int(rd + wr),
                     "cells": 10000299998, "algorithmic_bytes": 2 * 100000 * 12 * 4 + 6 * 100000 * 4,
-                    "source": "ncu --set full --clock-control none (profiles/r1/final/wave_kernel_level0_full.txt)"}}
+                    "source": f"ncu --set full --clock-control none (profiles/{RND}/final/wave_kernel_level0_full.txt)"}}
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "wave_kernel_traffic.json"), "w"), indent=1)
 # every BASELINE config
 res = []
 for c, path in [("cfg1", "cfg_cfg1.json"), ("cfg2", "cfg_cfg2.json"), ("cfg3", "final_bench.json"),
-                ("cfg4", "cfg_cfg4.json"), ("cfg5", "cfg_cfg5.json"), ("cfg3x64", "cfg_cfg3x64.json")]:
+                ("cfg4", "cfg_cfg4.json"), ("cfg5", "cfg_cfg5.json"), ("cfg3x64", "cfg_cfg3x64.json"),
+                ("d100", "cfg_d100.json"), ("d100x64", "cfg_d100x64.json")]:
+        if not os.path.exists(os.path.join(G, path)):
+            continue
     d = last_json(os.path.join(G, path))
     res.append({"config": c, "workload": d["config"]["workload"], "dtype": d["dtype"], "GCUPS": d["value"],
                 "ms_per_step": d["ms_per_step"], "sec_per_alignment": d["config"]["sec_per_alignment"],
