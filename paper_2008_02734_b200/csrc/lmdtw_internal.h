@@ -39,7 +39,7 @@ struct PassDesc {
 // persistent pipelines rotate over strips instead of holding one strip for
 // its whole length (a multiple of 32 and of the ring chunk).
 #ifndef LMDTW_TILE_W
-#define LMDTW_TILE_W 2048
+#define LMDTW_TILE_W 8192  // measured: 2048 -> 8192 cfg3 36.3 -> 35.75 ms, cfg4 353 -> 344 ms
 #endif
 constexpr int kTileW = LMDTW_TILE_W;
 
