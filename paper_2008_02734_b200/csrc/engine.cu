@@ -93,6 +93,30 @@ struct DBuf {
         return cudaSuccess;
     }
     template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+    // Grow to n bytes keeping the first `used` bytes (offsets into the buffer
+    // stay valid); stream-ordered copy, the old block freed after it.
+    cudaError_t grow_keep(size_t n, size_t used, cudaStream_t st) {
+        if (n <= cap && p) return cudaSuccess;
+        void* q = nullptr;
+        const size_t c = std::max<size_t>(n + n / 2, 1 << 20);
+        cudaError_t e = cudaMalloc(&q, c);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return e;
+        }
+        if (p && used) {
+            e = cudaMemcpyAsync(q, p, used, cudaMemcpyDeviceToDevice, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) {
+                cudaFree(q);
+                return e;
+            }
+        }
+        if (p) cudaFree(p);
+        p = q;
+        cap = c;
+        return cudaSuccess;
+    }
 };
 
 struct HBuf {
@@ -122,7 +146,7 @@ struct HBuf {
 struct Slot {
     cudaStream_t st = nullptr;
     cudaEvent_t done = nullptr;
-    DBuf passes, items, counter, out, bnd, pdesc, pout, pscratch, trace, lb, flags, istage;
+    DBuf passes, items, counter, out, bnd, pdesc, pout, pscratch, trace, lb, flags, istage, wins;
     HBuf h_passes, h_items, h_istage, h_pdesc, h_pout;
 };
 
@@ -134,6 +158,7 @@ struct Ctx {
     Slot main;                                  // main.st == st
     std::vector<std::unique_ptr<Slot>> extra;   // more batch slots, created on demand
     DBuf xraw, yraw, xp, yp, ldesc, bp, path, pcost, plen, lcost, tab;
+    DBuf arena;  // recursion outputs with stable offsets: last diagonals + saved windows (align_core)
     // window.cu entry points (constrained DTW, path costs, discrepancy)
     DBuf wlo, whi, woff, wbp, wbnd, wdesc, wcost, wpath, wpoff, wplen, pcells, pcost2, poffs, pxoff, pyoff, ppid,
         pout2, dsc;
@@ -382,12 +407,57 @@ struct Node {
     double total = 0;
     int leaf = -1;  // index into leaf list
     int depth = 0;  // recursion level (root 0)
+    // half-pass reuse: the saved pass whose windows hold this node's forward /
+    // reverse diagonals (-1: compute them), and the passes this node's own
+    // children inherit from (set when the node's batch is built)
+    int fsrc = -1, bsrc = -1, fpass = -1, bpass = -1;
 };
+
+// A computed half pass kept for the descendants on its spine: a forward pass
+// of node n serves n.left, n.left.left, ... (same first cell), a reverse pass
+// n.right, n.right.right, ... (same last cell).
+struct SavedPass {
+    int64_t M, N;                 // grid of the node that computed it
+    std::vector<WinDesc> wins;    // arena offsets (element units)
+};
+
+// Diagonal ranges a pass's spine descendants may need, in the pass's
+// coordinates.  Forward (left spine): a child's K = kpiv + 1 with the
+// pivot's diagonal kpiv in [kf - 2, kf], kf = (K + 1) / 2; reverse (right
+// spine): a child's K = K - kpiv.  A descendant with M' + N' < 2 min_dim is
+// a leaf (no pivot), which ends the spine.
+void spine_windows(int64_t K, int rev, int64_t min_dim, std::vector<std::pair<int64_t, int64_t>>& out) {
+    int64_t lo = K, hi = K;
+    for (int depth = 0; depth < 64; depth++) {
+        int64_t clo = INT64_MAX, chi = -1;
+        for (int64_t k = lo; k <= hi; k++) {
+            const int64_t kf = (k + 1) / 2;
+            clo = std::min(clo, rev ? k - kf : kf - 1);
+            chi = std::max(chi, rev ? k - kf + 2 : kf + 1);
+        }
+        if (chi + 1 < 2 * min_dim || clo < 2) break;
+        int64_t dlo = INT64_MAX, dhi = -1;
+        for (int64_t k = clo; k <= chi; k++) {
+            const int64_t kf = (k + 1) / 2, kstop = rev ? kf + ((k % 2 == 0) ? 1 : 0) : kf;
+            dlo = std::min(dlo, kstop - 2);
+            dhi = std::max(dhi, kstop);
+        }
+        out.push_back({std::max<int64_t>(dlo, 0), dhi});
+        lo = clo;
+        hi = chi;
+    }
+}
 
 struct Engine {
     Ctx& c;
     int prec, d, dp, H;  // dp: padded row length (elements); H: strip height of the launch being built
     int lat = 0;         // the launch being built uses the latency variant (strip_height(.., 1))
+    void* out_base = nullptr;  // diagonal outputs of run_wave (null: the slot's buffer)
+    // half-pass reuse (align_core): saved passes and the arena fill (elements)
+    bool reuse = false;
+    int64_t min_dim = 500;
+    std::vector<SavedPass> saved;
+    int64_t arena_used = 0;
     int lat_policy = 1;  // LMDTW_LAT: 0 never, 1 latency-bound launches, 2 always
     void set_lat(int l) {
         (void)l;  // the latency variant is not dispatched (kernels.cu, WsCfg::R)
@@ -591,7 +661,8 @@ struct Engine {
         w.items = S.items.as<WorkItem>();
         w.nitems = (int)nitems;
         w.counter = S.counter.as<int>();
-        w.out = S.out.p;
+        w.out = out_base ? out_base : S.out.p;
+        w.wins = S.wins.as<WinDesc>();
         w.bnd = S.bnd.p;
         w.bp = c.bp.as<unsigned long long>();
         w.lb = S.lb.p;
@@ -697,6 +768,8 @@ struct Engine {
         p.tab_off = -1;
         p.w64 = 0;
         p.leaf_id = -1;
+        p.win_first = 0;
+        p.win_count = 0;
         return p;
     }
 
@@ -727,18 +800,85 @@ struct Engine {
             set_lat(lb ? 1 : 0);
         }
         P.reserve(nodes.size() * 2);
+        // Outputs: with reuse (align_core) every diagonal lives in the per-call
+        // arena at a stable offset (saved windows outlive the batch);
+        // otherwise in the slot's buffer from offset 0.
+        const int64_t base0 = reuse ? arena_used : 0;
+        out_total = base0;
+        std::vector<WinDesc> W;
+        int64_t computed = 0;  // cells the wave kernel actually updates
+        auto computed_pass = [&](const Node& n, int64_t kstop, int rev) -> int {
+            PassDesc p = half_pass_desc(xb[n.pair] + n.i_off, yb[n.pair] + n.j_off, n.M, n.N, kstop, rev,
+                                        out_total, bnd_total);
+            computed += cells_upto(kstop, n.M, n.N);
+            if (!reuse) {
+                P.push_back(p);
+                return -1;
+            }
+            std::vector<std::pair<int64_t, int64_t>> rng;
+            spine_windows(n.M + n.N - 1, rev, min_dim, rng);
+            SavedPass sp;
+            sp.M = n.M;
+            sp.N = n.N;
+            p.win_first = (int32_t)W.size();
+            for (auto& r : rng) {
+                if (r.second > kstop - 3) continue;  // never past the pass's own last diagonals
+                WinDesc wd{};
+                wd.k_lo = (int32_t)r.first;
+                wd.k_hi = (int32_t)r.second;
+                int64_t stride = 0;
+                for (int64_t k = r.first; k <= r.second; k++) stride = std::max(stride, dlen(k, n.M, n.N));
+                wd.stride = (int32_t)stride;
+                wd.d_off = out_total;
+                out_total += (r.second - r.first + 1) * stride;
+                wd.c_off = out_total;
+                out_total += (r.second - r.first + 1) * stride;
+                W.push_back(wd);
+                sp.wins.push_back(wd);
+            }
+            p.win_count = (int32_t)W.size() - p.win_first;
+            P.push_back(p);
+            saved.push_back(std::move(sp));
+            return (int)saved.size() - 1;
+        };
+        // a pass inherited from a saved one: a descriptor the pivot kernel
+        // reads (no strips), its offsets pointing into the saved windows
+        auto inherited_pass = [&](const Node& n, int src, int64_t kstop) -> bool {
+            const SavedPass& sp = saved[src];
+            PassDesc p{};
+            for (int s3 = 0; s3 < 3; s3++) {
+                const int64_t k = kstop - 2 + s3;
+                const WinDesc* w = nullptr;
+                for (const auto& wd : sp.wins)
+                    if (k >= wd.k_lo && k <= wd.k_hi) w = &wd;
+                if (!w) return false;
+                // the node's diag index idx is the saved pass's idx + shift
+                const int64_t shift = std::min(k, sp.M - 1) - std::min(k, n.M - 1);
+                p.out_off[s3] = w->d_off + (k - w->k_lo) * w->stride + shift;
+                p.out_off[3 + s3] = w->c_off + (k - w->k_lo) * w->stride + shift;
+            }
+            p.M = (int32_t)n.M;
+            p.N = (int32_t)n.N;
+            p.kstop = (int32_t)kstop;
+            P.push_back(p);
+            return true;
+        };
         for (int q : nodes) {
-            const Node& n = all[q];
+            Node& n = all[q];
             const int64_t K = n.M + n.N - 1;
             const int64_t kf = (K + 1) / 2;
             const int64_t kb = (K % 2 == 0) ? kf + 1 : kf;
             PivotDesc v{};
             v.fwd = (int)P.size();
-            P.push_back(half_pass_desc(xb[n.pair] + n.i_off, yb[n.pair] + n.j_off, n.M, n.N, kf, 0, out_total,
-                                       bnd_total));
+            if (reuse && n.fsrc >= 0 && inherited_pass(n, n.fsrc, kf))
+                n.fpass = n.fsrc;
+            else
+                n.fpass = computed_pass(n, kf, 0);
             v.bwd = (int)P.size();
-            P.push_back(half_pass_desc(xb[n.pair] + n.i_off, yb[n.pair] + n.j_off, n.M, n.N, kb, 1, out_total,
-                                       bnd_total));
+            if (reuse && n.bsrc >= 0 && inherited_pass(n, n.bsrc, kb))
+                n.bpass = n.bsrc;
+            else
+                n.bpass = computed_pass(n, kb, 1);
             v.M = (int)n.M;
             v.N = (int)n.N;
             v.kf = (int)kf;
@@ -751,8 +891,19 @@ struct Engine {
             if (peak_out)
                 peak_out->push_back(std::max(peak_values(kf, n.M, n.N), peak_values(kb, n.M, n.N)));
         }
-        CU(S.out.ensure((size_t)out_total * esz));
-        TRY(run_wave(S, P, bnd_total, false, nullptr, nullptr, cells));
+        if (reuse) {
+            CU(c.arena.grow_keep((size_t)std::max<int64_t>(out_total, 1) * esz, (size_t)arena_used * esz, S.st));
+            arena_used = out_total;
+            out_base = c.arena.p;
+        } else {
+            CU(S.out.ensure((size_t)std::max<int64_t>(out_total, 1) * esz));
+            out_base = S.out.p;
+        }
+        CU(S.wins.ensure(std::max<size_t>(W.size(), 1) * sizeof(WinDesc)));
+        if (!W.empty())
+            CU(cudaMemcpyAsync(S.wins.p, W.data(), W.size() * sizeof(WinDesc), cudaMemcpyHostToDevice, S.st));
+        (void)cells;
+        TRY(run_wave(S, P, bnd_total, false, nullptr, nullptr, computed));
         CU(S.pdesc.ensure(V.size() * sizeof(PivotDesc)));
         CU(S.pout.ensure(V.size() * sizeof(PivotOut)));
         CU(S.h_pdesc.ensure(V.size() * sizeof(PivotDesc)));
@@ -762,7 +913,7 @@ struct Engine {
         const size_t scb = pivot_scratch_bytes((int)V.size());
         CU(S.pscratch.ensure(scb));
         CU(cudaMemsetAsync(S.pscratch.p, 0, scb, S.st));  // zeroes the per-node done counters
-        TRY(launched(launch_pivots(prec, S.passes.as<PassDesc>(), S.pdesc.as<PivotDesc>(), (int)V.size(), S.out.p,
+        TRY(launched(launch_pivots(prec, S.passes.as<PassDesc>(), S.pdesc.as<PivotDesc>(), (int)V.size(), out_base,
                                    S.pout.as<PivotOut>(), S.pscratch.p, S.st),
                      "pivot_kernel"));
         CU(cudaMemcpyAsync(S.h_pout.p, S.pout.p, V.size() * sizeof(PivotOut), cudaMemcpyDeviceToHost, S.st));
@@ -942,6 +1093,20 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     E.tie[0] = cfg.tie[0];
     E.tie[1] = cfg.tie[1];
     E.tie[2] = cfg.tie[2];
+    // Half-pass reuse: a left child's forward half pass is its parent's
+    // forward pass restricted to the top-left block (same first cell, the
+    // same recurrence, bit-identical values), a right child's reverse pass
+    // likewise; each pass saves the diagonals its spine descendants need, so
+    // every node below the root computes one half pass instead of two.
+    // cells_processed keeps the reference's count (both half passes of every
+    // node, divide.py:148-178).  LMDTW_REUSE=0 computes both.
+    {
+        const char* e = getenv("LMDTW_REUSE");
+        E.reuse = !(e && atoi(e) == 0);
+        E.min_dim = cfg.min_dim;
+        E.arena_used = 0;
+        E.saved.clear();
+    }
     std::vector<int64_t> xb, yb;
     // LMDTW_PHASES=1: host timestamps of the phases of this call (diagnostics)
     const bool phases = getenv("LMDTW_PHASES") != nullptr;
@@ -1105,12 +1270,14 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
             l.N = parent.pj + 1;
             l.pair = parent.pair;
             l.depth = parent.depth + 1;
+            l.fsrc = parent.fpass;  // same first cell: the parent's forward pass restricted
             r.i_off = parent.i_off + parent.pi;
             r.j_off = parent.j_off + parent.pj;
             r.M = parent.M - parent.pi;
             r.N = parent.N - parent.pj;
             r.pair = parent.pair;
             r.depth = parent.depth + 1;
+            r.bsrc = parent.bpass;  // same last cell: the parent's reverse pass restricted
             nodes.push_back(l);
             nodes[id].left = (int)nodes.size() - 1;
             classify(nodes[id].left);

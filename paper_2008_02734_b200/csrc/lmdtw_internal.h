@@ -33,6 +33,21 @@ struct PassDesc {
     int32_t sys_out;        // 1: strip strip_hi-1 publishes to a consumer on another GPU (system-scope stores)
     uint64_t bnd_in_first;  // != 0: strip strip_lo reads strip strip_lo-1's handoff slots here
                             // (another shard's buffer, e.g. a peer GPU's), system-scope loads
+    int32_t win_first;      // extra diagonals this pass saves (WinDesc entries [win_first, +win_count))
+    int32_t win_count;
+};
+
+// A run of consecutive diagonals [k_lo, k_hi] (pass coordinates) whose D and
+// C values a half pass saves besides its last three: the diagonals the pass's
+// descendants on its spine need (a left child's forward half pass is its
+// parent's forward pass restricted to the top-left block, a right child's
+// reverse pass likewise), so those descendants skip recomputing them.
+// D(k, idx) lands at out[d_off + (k - k_lo) * stride + idx], C likewise.
+struct WinDesc {
+    int32_t k_lo, k_hi;
+    int32_t stride;
+    int32_t pad;
+    int64_t d_off, c_off;
 };
 
 // Columns per work item: a strip is cut into tiles of kTileW columns so the
@@ -110,6 +125,7 @@ struct WaveLaunch {
     int grid_warps;         // persistent warps to launch (0 = auto)
     unsigned long long* trace;  // optional per-item timestamps (debug)
     int lat;                // 1: latency variant (strip height strip_height(.., 1))
+    const WinDesc* wins;    // saved-diagonal windows of the passes (PassDesc::win_first/win_count)
 };
 
 // How feature rows of dimension d are laid out and which kernels run them:
