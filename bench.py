@@ -9,7 +9,11 @@ full alignment.  Metric: GCUPS = cells_processed / s (the reference's own
 counter, ~2*M*N), plus seconds per alignment.
 
 value  : inputs resident in HBM (device pointers through the C ABI), CUDA
-         events on the library's stream, L2 flushed between steps.
+         events on the library's stream, L2 flushed between steps.  Cells are
+         the reference's cells_processed counter (both half passes of every
+         node, ~2MN); the engine updates fewer (a child inherits one of its two
+         half passes from its parent): config.cells_computed_per_step, which
+         the roofline uses.
 e2e    : the public drop-in call linmdtw(FeatureSeries, ...) on pinned host
          buffers: H2D copies, all kernels, path D2H and host stitching timed.
 roofline: the strip-wavefront kernel's cell updates/s (CUDA events around
@@ -514,7 +518,9 @@ def run_ours(args, rank, world):
         "scaling": "strong" if dist_single else "weak", "vs_baseline": None,
         "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
         "config": {"workload": cfgd["workload"], "min_dim": args.min_dim, "precision": prec,
-                   "cells_per_step": cells // args.steps, "sec_per_alignment": round(step_ms / 1e3 / n_total, 6),
+                   "cells_per_step": cells // args.steps,
+                   "cells_computed_per_step": (prof["wave_cells"] + prof["leaf_cells"]) // args.steps,
+                   "sec_per_alignment": round(step_ms / 1e3 / n_total, 6),
                    "l2": "flushed (256 MiB write) between timed steps", "parallelism": ("single-gpu" if world == 1 else
                                    (f"level-sharded x{world} (one alignment, distributed.py)" if dist_single
                                     else f"pairs sharded longest-first over {world} ranks"))},

@@ -817,6 +817,7 @@ struct Engine {
             }
             std::vector<std::pair<int64_t, int64_t>> rng;
             spine_windows(n.M + n.N - 1, rev, min_dim, rng);
+            std::sort(rng.begin(), rng.end());  // the kernel walks windows in increasing k
             SavedPass sp;
             sp.M = n.M;
             sp.N = n.N;
