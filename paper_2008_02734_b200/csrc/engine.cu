@@ -455,6 +455,7 @@ struct Engine {
     void* out_base = nullptr;  // diagonal outputs of run_wave (null: the slot's buffer)
     // half-pass reuse (align_core): saved passes and the arena fill (elements)
     bool reuse = false;
+    int windows_policy = 1;  // LMDTW_WINDOWS: 1 not for latency-bound batches, 2 always
     int64_t min_dim = 500;
     std::vector<SavedPass> saved;
     int64_t arena_used = 0;
@@ -807,11 +808,26 @@ struct Engine {
         out_total = base0;
         std::vector<WinDesc> W;
         int64_t computed = 0;  // cells the wave kernel actually updates
+        // Windows put stores on the strips' DP path: a latency-bound batch
+        // (its head strips set the time) saves none -- its children then
+        // compute both half passes (inherited_pass finds no window).
+        bool save_windows = reuse;
+        if (reuse && windows_policy == 1) {
+            std::vector<PassDesc> probe;
+            int64_t o = 0, bt = 0;
+            for (int q : nodes) {
+                const Node& n = all[q];
+                const int64_t K = n.M + n.N - 1, kf = (K + 1) / 2, kb = (K % 2 == 0) ? kf + 1 : kf;
+                if (!(n.fsrc >= 0)) probe.push_back(half_pass_desc(0, 0, n.M, n.N, kf, 0, o, bt));
+                if (!(n.bsrc >= 0)) probe.push_back(half_pass_desc(0, 0, n.M, n.N, kb, 1, o, bt));
+            }
+            save_windows = !latency_bound(probe);
+        }
         auto computed_pass = [&](const Node& n, int64_t kstop, int rev) -> int {
             PassDesc p = half_pass_desc(xb[n.pair] + n.i_off, yb[n.pair] + n.j_off, n.M, n.N, kstop, rev,
                                         out_total, bnd_total);
             computed += cells_upto(kstop, n.M, n.N);
-            if (!reuse) {
+            if (!save_windows) {
                 P.push_back(p);
                 return -1;
             }
@@ -1104,6 +1120,8 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     {
         const char* e = getenv("LMDTW_REUSE");
         E.reuse = !(e && atoi(e) == 0);
+        const char* w = getenv("LMDTW_WINDOWS");
+        E.windows_policy = w ? atoi(w) : 1;
         E.min_dim = cfg.min_dim;
         E.arena_used = 0;
         E.saved.clear();
