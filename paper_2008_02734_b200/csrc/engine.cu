@@ -147,7 +147,7 @@ struct Slot {
     cudaStream_t st = nullptr;
     cudaEvent_t done = nullptr;
     DBuf passes, items, counter, out, bnd, pdesc, pout, pscratch, trace, lb, flags, istage, wins;
-    HBuf h_passes, h_items, h_istage, h_pdesc, h_pout;
+    HBuf h_passes, h_items, h_istage, h_pdesc, h_pout, h_wins;
 };
 
 struct Ctx {
@@ -917,8 +917,11 @@ struct Engine {
             out_base = S.out.p;
         }
         CU(S.wins.ensure(std::max<size_t>(W.size(), 1) * sizeof(WinDesc)));
-        if (!W.empty())
-            CU(cudaMemcpyAsync(S.wins.p, W.data(), W.size() * sizeof(WinDesc), cudaMemcpyHostToDevice, S.st));
+        if (!W.empty()) {  // through pinned staging: a pageable copy would block the host
+            CU(S.h_wins.ensure(W.size() * sizeof(WinDesc)));
+            memcpy(S.h_wins.p, W.data(), W.size() * sizeof(WinDesc));
+            CU(cudaMemcpyAsync(S.wins.p, S.h_wins.p, W.size() * sizeof(WinDesc), cudaMemcpyHostToDevice, S.st));
+        }
         (void)cells;
         TRY(run_wave(S, P, bnd_total, false, nullptr, nullptr, computed));
         CU(S.pdesc.ensure(V.size() * sizeof(PivotDesc)));
