@@ -833,6 +833,21 @@ struct Engine {
             }
             std::vector<std::pair<int64_t, int64_t>> rng;
             spine_windows(n.M + n.N - 1, rev, min_dim, rng);
+            // A window costs every strip of this pass ~8 chunks of stores on
+            // its DP path; it saves one half pass of a descendant whose
+            // M' + N' ~ 2 * (the window's middle k): keep it only where the
+            // saved cells outweigh ~2x the cells of those chunks (measured:
+            // storing all 8 windows of cfg3's root passes cost 3.6% of level 0)
+            {
+                const double cost = 2.0 * p.nstrips * 8.0 * 16.0 * H;
+                std::vector<std::pair<int64_t, int64_t>> keep;
+                for (auto& r : rng) {
+                    const double half = (double)(r.first + r.second) / 2.0;  // ~ the descendant's kf ~ (M'+N')/2
+                    const double saved_cells = half * half / 2.0;          // its half pass, ~square
+                    if (saved_cells > cost) keep.push_back(r);
+                }
+                rng.swap(keep);
+            }
             std::sort(rng.begin(), rng.end());  // the kernel walks windows in increasing k
             SavedPass sp;
             sp.M = n.M;
