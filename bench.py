@@ -533,7 +533,11 @@ def run_ours(args, rank, world):
                      "peak": round(roof / 1e9, 2), "unit": "Gcell/s", "frac": round(wave_rate / roof, 4),
                      "traffic": traffic, "traffic_basis": traffic_basis,
                      "peak_basis": f"N_SM={n_sm} x 128 lanes x {f_mhz} MHz ({kind} sm_max_mhz) / (2d+5), d={d}",
-                     "kernel_ms_share": round(prof["wave_ms"] / sum(ms), 4) if sum(ms) > 0 else None},
+                     "kernel_ms_share": round(prof["wave_ms"] / sum(ms), 4) if sum(ms) > 0 else None,
+                     # the alignment's rate in the reference's cell count (value) against the same peak:
+                     # the kernel's frac above counts only the cells it updates (a child inherits one
+                     # of its two half passes), this one what an alignment is worth
+                     "frac_alignment": round(value * 1e9 / roof, 4)},
         "clocks": clocks,
         "gpu_launches": launches,
     }

@@ -70,13 +70,15 @@ res = []
 for c, path in [("cfg1", "cfg_cfg1.json"), ("cfg2", "cfg_cfg2.json"), ("cfg3", "final_bench.json"),
                 ("cfg4", "cfg_cfg4.json"), ("cfg5", "cfg_cfg5.json"), ("cfg3x64", "cfg_cfg3x64.json"),
                 ("d100", "cfg_d100.json"), ("d100x64", "cfg_d100x64.json")]:
-        if not os.path.exists(os.path.join(G, path)):
-            continue
+    if not os.path.exists(os.path.join(G, path)):
+        continue
     d = last_json(os.path.join(G, path))
     res.append({"config": c, "workload": d["config"]["workload"], "dtype": d["dtype"], "GCUPS": d["value"],
                 "ms_per_step": d["ms_per_step"], "sec_per_alignment": d["config"]["sec_per_alignment"],
                 "e2e_GCUPS": d["e2e"]["value"], "wave_kernel_Gcell_s": d["roofline"]["achieved"],
-                "roofline_frac_fp32_slots": d["roofline"]["frac"], "clocks": d.get("clocks")})
+                "roofline_frac_fp32_slots": d["roofline"]["frac"], "clocks": d.get("clocks"),
+                "cells_per_step": d["config"]["cells_per_step"],
+                "cells_computed_per_step": d["config"].get("cells_computed_per_step")})
 ref = last_json(os.path.join(G, "final_reference.json"))
 json.dump({"gpu": "1x B200", "command": "python bench.py (cfg3) / --config <cfg> --steps 3 --warmup 1 --no-cpu",
            "results": res, "reference_arm": ref}, open(os.path.join(OUT, "configs.json"), "w"), indent=1)
