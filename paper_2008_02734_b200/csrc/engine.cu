@@ -767,7 +767,7 @@ struct Engine {
         p.sys_out = 0;
         p.bp_off = 0;
         p.tab_off = -1;
-        p.w64 = 0;
+        p.bp_ld = 0;
         p.leaf_id = -1;
         p.win_first = 0;
         p.win_count = 0;
@@ -1011,9 +1011,11 @@ struct Engine {
             p.sys_out = 0;
             p.bnd_off = bnd_total;
             bnd_total += 2 * ((nd.N + 1) & ~1LL) * bwords();  // two slots, 16-byte aligned
-            p.w64 = (int32_t)((nd.N + 31) / 32);
+            // block-major words: block jw of row i at bp_off + jw * bp_ld + i,
+            // rows padded to whole strips (a strip's row-less lanes store too)
+            p.bp_ld = (int32_t)(p.nstrips * H);
             p.bp_off = bp_total;
-            bp_total += nd.M * p.w64;
+            bp_total += (int64_t)p.bp_ld * ((nd.N + 31) / 32);
             p.tab_off = tab_host ? 0 : -1;
             p.leaf_id = q;
             LeafDesc& l = L[q];
@@ -1025,7 +1027,7 @@ struct Engine {
             l.pass = q;
             l.path_off = path_total;
             l.bp_off = p.bp_off;
-            l.w64 = p.w64;
+            l.bp_ld = p.bp_ld;
             path_off[q] = path_total;
             path_total += nd.M + nd.N - 1;
             cells += nd.M * nd.N;

@@ -23,7 +23,7 @@ struct PassDesc {
     int64_t bnd_off;        // 2 slots x N tagged 64-bit words (x2 for fp64): strip handoff
     int64_t bp_off;         // leaf: backpointer words (uint64, 32 cells each)
     int64_t tab_off;        // leaf: optional full D table (-1 = none)
-    int32_t w64;            // leaf: words per backpointer row = ceil(N/32)
+    int32_t bp_ld;          // leaf: backpointer words per 32-column block (nstrips * H rows; block-major)
     int32_t leaf_id;        // leaf: index into per-leaf outputs
     int64_t lb_off;         // tile left boundaries: nstrips x (H + 1) values (set by the launcher)
     int64_t flag_off;       // tiles completed per strip: nstrips ints (set by the launcher)
@@ -96,7 +96,7 @@ struct LeafDesc {
     int32_t pad;
     int64_t path_off;       // capacity M+N-1 (i,j) int32 pairs, written reversed
     int64_t bp_off;
-    int32_t w64;
+    int32_t bp_ld;          // words per 32-column block (PassDesc::bp_ld)
     int32_t pad2;
 };
 

@@ -4,8 +4,10 @@ import numpy as np
 
 PD = np.dtype([("x_off", "<i8"), ("y_off", "<i8"), ("M", "<i4"), ("N", "<i4"), ("kstop", "<i4"), ("reverse", "<i4"),
                ("rows", "<i4"), ("nstrips", "<i4"), ("out_off", "<i8", 6), ("bnd_off", "<i8"), ("bp_off", "<i8"),
-               ("tab_off", "<i8"), ("w64", "<i4"), ("leaf_id", "<i4"), ("lb_off", "<i8"),
-               ("flag_off", "<i8"), ("tile_w", "<i4"), ("pad", "<i4")])
+               ("tab_off", "<i8"), ("bp_ld", "<i4"), ("leaf_id", "<i4"), ("lb_off", "<i8"),
+               ("flag_off", "<i8"), ("tile_w", "<i4"), ("strip_lo", "<i4"), ("strip_hi", "<i4"),
+               ("sys_out", "<i4"), ("bnd_in_first", "<u8"), ("win_first", "<i4"), ("win_count", "<i4")])
+assert PD.itemsize == 168
 WI = np.dtype([("pass", "<i4"), ("strip", "<i4"), ("blk", "<i4"), ("pad", "<i4")])
 
 
@@ -43,7 +45,7 @@ for li, (P, I, T, leaf, B) in enumerate(launches(sys.argv[1])):
     rpace = run * 1e3 * 1.965 / steps
     print(f"   boundary wait: mean {wait.mean():.1f} us (b>0: {wait[b > 0].mean():.1f}); run pace median {np.median(rpace):.0f} "
           f"mean {np.average(rpace, weights=steps):.0f} p90 {np.percentile(rpace, 90):.0f}; wait share {wait.sum() / dur.sum():.2f}")
-    if li == 0:
+    if li == 0 or leaf:
         # time histogram of concurrently running items
         ts = np.linspace(0, span * 1e6, 21)
         conc = [int(((T[:, 0] - t0 <= t) & (T[:, 1] - t0 > t)).sum()) for t in ts]
