@@ -92,6 +92,15 @@ struct DBuf {
         cap = c;
         return cudaSuccess;
     }
+    // ensure, and fill a new allocation with `byte` (buffers the kernels
+    // leave clean after every launch: queue counters, tile flags, pivot
+    // counters; handoff words, whose stale tags never match -- Engine::next_tags)
+    cudaError_t ensure_init(size_t n, int byte, cudaStream_t st) {
+        if (n <= cap && p) return cudaSuccess;
+        cudaError_t e = ensure(n);
+        if (e == cudaSuccess) e = cudaMemsetAsync(p, byte, cap, st);
+        return e;
+    }
     template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
     // Grow to n bytes keeping the first `used` bytes (offsets into the buffer
     // stay valid); stream-ordered copy, the old block freed after it.
@@ -143,15 +152,40 @@ struct HBuf {
 // One in-flight batch of half passes (a set of recursion nodes): its stream
 // and its buffers.  Batches run concurrently on their own streams, so the
 // children of a node start while other nodes of its level still run.
+// Host side of one host->device upload per launch batch: pass descriptors,
+// the tile queue's build input, saved-window and pivot descriptors, packed at
+// 16-byte aligned offsets (Engine::upload).
+struct Staging {
+    std::vector<char> h;
+    size_t reserve(size_t n) {
+        const size_t o = (h.size() + 15) & ~(size_t)15;
+        h.resize(o + n);
+        return o;
+    }
+    size_t add(const void* src, size_t n) {
+        const size_t o = reserve(n);
+        if (n) memcpy(h.data() + o, src, n);
+        return o;
+    }
+    template <typename T> T* at(size_t o) { return reinterpret_cast<T*>(h.data() + o); }
+};
+
 struct Slot {
     cudaStream_t st = nullptr;
     cudaEvent_t done = nullptr;
-    DBuf passes, items, counter, out, bnd, pdesc, pout, pscratch, trace, lb, flags, istage, wins;
+    DBuf passes, items, counter, out, bnd, pdesc, pout, pscratch, pdone, trace, lb, flags, istage, wins;
     HBuf h_passes, h_items, h_istage, h_pdesc, h_pout, h_wins;
+    Staging stg;       // the batch being built
+    HBuf h_stage;      // its pinned copy
+    DBuf d_stage;      // its device copy (valid until the slot's next upload)
+    size_t passes_off = 0;  // PassDesc array of the last run_wave in d_stage
+    int tag_next = 0;       // next free handoff tag base of `bnd`
+    template <typename T> T* dev(size_t off) const { return reinterpret_cast<T*>((char*)d_stage.p + off); }
 };
 
 struct Ctx {
     int device = 0;
+    int nsm = 148;  // SMs of the device
     std::mutex mu;
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -162,7 +196,15 @@ struct Ctx {
     // window.cu entry points (constrained DTW, path costs, discrepancy)
     DBuf wlo, whi, woff, wbp, wbnd, wdesc, wcost, wpath, wpoff, wplen, pcells, pcost2, poffs, pxoff, pyoff, ppid,
         pout2, dsc;
-    HBuf h_path, h_pcost, h_plen, h_lcost;
+    // leaf outputs, one device block and its pinned copy (one D2H copy):
+    // reversed local paths (int pairs) | per-cell costs | lengths | D(M-1, N-1)
+    DBuf lout;
+    HBuf h_lout;
+    size_t lo_pcost = 0, lo_plen = 0, lo_lcost = 0;
+    const int* hpath() const { return h_lout.as<int>(); }
+    template <typename T> const T* hpcost() const { return reinterpret_cast<const T*>(h_lout.as<char>() + lo_pcost); }
+    const int* hplen() const { return reinterpret_cast<const int*>(h_lout.as<char>() + lo_plen); }
+    template <typename T> const T* hlcost() const { return reinterpret_cast<const T*>(h_lout.as<char>() + lo_lcost); }
     long long call_launches = 0;
     long long h2d = 0, d2h = 0;
     // profiling (lmdtw_profile_enable): events around wave launches, read
@@ -262,6 +304,7 @@ int make_ctx(int device, std::unique_ptr<Ctx>& out) {
     std::unique_ptr<Ctx> c(new Ctx());
     c->device = device;
     CU(cudaSetDevice(device));
+    CU(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
     CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     CU(cudaEventCreate(&c->ev0));
     CU(cudaEventCreate(&c->ev1));
@@ -469,8 +512,7 @@ struct Engine {
     // than the launch has tiles per pipeline (twice over): the head strips'
     // chain, not the FMA pipes, then sets the time.
     bool latency_bound(const std::vector<PassDesc>& P) {
-        int nsm = 148;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
+        const int nsm = c.nsm;
         int64_t head = 0, tiles = 0;
         for (const auto& p : P) {
             head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
@@ -559,7 +601,8 @@ struct Engine {
     // exclusive prefix sum is each key's first queue slot.  The tiles
     // themselves are scattered on the device (scatter_items_kernel), so the
     // host never touches the O(tiles) queue.  Returns the number of tiles.
-    int64_t stage_items(Slot& S, const std::vector<PassDesc>& P, int64_t& nents, int64_t& nkeys) {
+    int64_t stage_items(Slot& S, const std::vector<PassDesc>& P, int64_t& nents, int64_t& nkeys, size_t& ents_off,
+                        size_t& cur_off) {
         const int64_t kPer = kTileW / lag_key();
         int64_t mmax = 0, total = 0;
         nents = 0;
@@ -572,10 +615,10 @@ struct Engine {
             }
         }
         nkeys = mmax + 1;
-        const size_t ent_bytes = (size_t)nents * sizeof(StripEnt);
-        CU(S.h_istage.ensure(ent_bytes + (size_t)(nkeys + kPer) * sizeof(int32_t)));
-        StripEnt* ents = S.h_istage.as<StripEnt>();
-        int32_t* cnt = reinterpret_cast<int32_t*>(S.h_istage.as<char>() + ent_bytes);
+        ents_off = S.stg.reserve((size_t)nents * sizeof(StripEnt));
+        cur_off = S.stg.reserve((size_t)(nkeys + kPer) * sizeof(int32_t));
+        StripEnt* ents = S.stg.at<StripEnt>(ents_off);
+        int32_t* cnt = S.stg.at<int32_t>(cur_off);
         std::fill(cnt, cnt + nkeys + kPer, 0);
         int64_t e = 0;
         for (size_t q = 0; q < P.size(); q++)
@@ -596,20 +639,62 @@ struct Engine {
         return total;
     }
 
-    // Build the tile queue of passes P in S.items (device), on c.st.
-    int upload_queue(Slot& S, const std::vector<PassDesc>& P, int64_t& nitems) {
-        int64_t nents = 0, nkeys = 0;
-        nitems = stage_items(S, P, nents, nkeys);
-        if (nitems < 0 || nitems > INT32_MAX) return set_err(LMDTW_EINTERNAL, "tile queue size");
-        const size_t ent_bytes = (size_t)nents * sizeof(StripEnt);
-        const size_t stage_bytes = ent_bytes + (size_t)nkeys * sizeof(int32_t);
-        CU(S.items.ensure((size_t)std::max<int64_t>(nitems, 1) * sizeof(WorkItem)));
-        CU(S.istage.ensure(stage_bytes));
-        CU(cudaMemcpyAsync(S.istage.p, S.h_istage.p, stage_bytes, cudaMemcpyHostToDevice, S.st));
-        return launched(launch_scatter_items(S.istage.as<StripEnt>(), (int)nents,
-                                             reinterpret_cast<int32_t*>(S.istage.as<char>() + ent_bytes),
+    // The slot's staged batch to the device: one pinned copy, one H2D copy on
+    // the slot's stream; the staging is then empty for the next batch.  (The
+    // slot's previous batch has completed: callers sync on it first.)
+    int upload(Slot& S) {
+        const size_t n = std::max<size_t>(S.stg.h.size(), 16);
+        CU(S.h_stage.ensure(n));
+        memcpy(S.h_stage.p, S.stg.h.data(), S.stg.h.size());
+        CU(S.d_stage.ensure(n));
+        CU(cudaMemcpyAsync(S.d_stage.p, S.h_stage.p, S.stg.h.size(), cudaMemcpyHostToDevice, S.st));
+        S.stg.h.clear();
+        return LMDTW_OK;
+    }
+
+    // Tile queue of passes P (staged, not yet uploaded): the scatter kernel
+    // runs after upload() from the offsets recorded here.
+    struct QueueStage {
+        int64_t nitems = 0, nents = 0;
+        size_t ents_off = 0, cur_off = 0;
+    };
+    int stage_queue(Slot& S, const std::vector<PassDesc>& P, QueueStage& q) {
+        int64_t nkeys = 0;
+        q.nitems = stage_items(S, P, q.nents, nkeys, q.ents_off, q.cur_off);
+        if (q.nitems < 0 || q.nitems > INT32_MAX) return set_err(LMDTW_EINTERNAL, "tile queue size");
+        CU(S.items.ensure((size_t)std::max<int64_t>(q.nitems, 1) * sizeof(WorkItem)));
+        return LMDTW_OK;
+    }
+    int scatter_queue(Slot& S, const QueueStage& q) {
+        return launched(launch_scatter_items(S.dev<StripEnt>(q.ents_off), (int)q.nents, S.dev<int32_t>(q.cur_off),
                                              (int)(kTileW / lag_key()), S.items.as<WorkItem>(), S.st),
                         "scatter_items_kernel");
+    }
+
+    // Build the tile queue of passes P in S.items (device), on S.st (entry
+    // points that upload their own descriptors).
+    int upload_queue(Slot& S, const std::vector<PassDesc>& P, int64_t& nitems) {
+        QueueStage q;
+        TRY(stage_queue(S, P, q));
+        TRY(upload(S));
+        nitems = q.nitems;
+        return scatter_queue(S, q);
+    }
+
+    // Handoff tags of a launch over `bnd`: strip a of the launch tags its words
+    // tag_base + a, above every tag an earlier launch on the buffer used, so
+    // stale words never match and the buffer needs no reset between launches
+    // (a new allocation is all tag -1; the base restarts, with a reset, near
+    // 2^30).
+    int next_tags(Slot& S, int64_t nstrips_max, int& tag_base) {
+        const int64_t span = nstrips_max + 2;
+        if ((int64_t)S.tag_next + span >= (1LL << 30)) {
+            CU(cudaMemsetAsync(S.bnd.p, 0xFF, S.bnd.cap, S.st));
+            S.tag_next = 0;
+        }
+        tag_base = S.tag_next;
+        S.tag_next += (int)span;
+        return LMDTW_OK;
     }
 
     // Host-built queue (debug entry points only): same order as the device
@@ -617,8 +702,10 @@ struct Engine {
     void make_items(Slot& S, const std::vector<PassDesc>& P, std::vector<WorkItem>& items) {
         const int64_t kPer = kTileW / lag_key();
         int64_t nents = 0, nkeys = 0;
-        const int64_t total = stage_items(S, P, nents, nkeys);
-        std::vector<int32_t> cur(S.h_istage.as<int32_t>() + nents * 3, S.h_istage.as<int32_t>() + nents * 3 + nkeys);
+        size_t ents_off = 0, cur_off = 0;
+        const int64_t total = stage_items(S, P, nents, nkeys, ents_off, cur_off);
+        std::vector<int32_t> cur(S.stg.at<int32_t>(cur_off), S.stg.at<int32_t>(cur_off) + nkeys);
+        S.stg.h.clear();
         items.resize(std::max<int64_t>(total, 0));
         for (size_t q = 0; q < P.size(); q++)
             for (int a = P[q].strip_lo; a < P[q].strip_hi; a++)
@@ -626,8 +713,14 @@ struct Engine {
                     items[cur[b * kPer + a]++] = WorkItem{(int)q, a, (int)b, 0};
     }
 
+    // One wave launch over passes P0: stages its descriptors and tile queue
+    // after whatever the caller staged in S.stg (wins_off: the caller's
+    // WinDesc array there, or npos), uploads the batch in one copy, builds the
+    // queue and launches.  The batch's device offsets stay valid until the
+    // slot's next upload (S.passes_off: the PassDesc array).
+    static constexpr size_t npos = ~(size_t)0;
     int run_wave(Slot& S, const std::vector<PassDesc>& P0, int64_t bnd_total, bool leaf, void* tab, void* lcost,
-                 int64_t cells) {
+                 int64_t cells, size_t wins_off = npos) {
         const auto th0 = std::chrono::steady_clock::now();
         // tile bookkeeping: per strip H+1 boundary values and a completion count
         std::vector<PassDesc> P(P0);
@@ -639,31 +732,35 @@ struct Engine {
             lb_total += (int64_t)p.nstrips * (H + 1);
             flag_total += p.nstrips;
         }
+        // buffers the kernel leaves clean (flags, counters) or never needs
+        // clean (handoff words, by their tags): initialised at allocation only
         CU(S.lb.ensure((size_t)std::max<int64_t>(lb_total, 1) * esz));
-        CU(S.flags.ensure((size_t)std::max<int64_t>(flag_total, 1) * sizeof(int)));
-        CU(cudaMemsetAsync(S.flags.p, 0, (size_t)std::max<int64_t>(flag_total, 1) * sizeof(int), S.st));
-        CU(S.h_passes.ensure(P.size() * sizeof(PassDesc)));
-        memcpy(S.h_passes.p, P.data(), P.size() * sizeof(PassDesc));
-        CU(S.passes.ensure(P.size() * sizeof(PassDesc)));
-        CU(S.counter.ensure(sizeof(int)));
-        CU(S.bnd.ensure((size_t)bnd_total * 8));
-        CU(cudaMemcpyAsync(S.passes.p, S.h_passes.p, P.size() * sizeof(PassDesc), cudaMemcpyHostToDevice, S.st));
-        int64_t nitems = 0;
-        TRY(upload_queue(S, P, nitems));
-        CU(cudaMemsetAsync(S.counter.p, 0, sizeof(int), S.st));
-        CU(cudaMemsetAsync(S.bnd.p, 0xFF, (size_t)bnd_total * 8, S.st));  // tag -1
+        CU(S.flags.ensure_init((size_t)std::max<int64_t>(flag_total, 1) * sizeof(int), 0, S.st));
+        CU(S.counter.ensure_init(2 * sizeof(int), 0, S.st));
+        CU(S.bnd.ensure_init((size_t)std::max<int64_t>(bnd_total, 1) * 8, 0xFF, S.st));
+        int64_t smax = 0;
+        for (const auto& p : P) smax = std::max<int64_t>(smax, p.nstrips);
+        int tag_base = 0;
+        TRY(next_tags(S, smax, tag_base));
+        S.passes_off = S.stg.add(P.data(), P.size() * sizeof(PassDesc));
+        QueueStage qs;
+        TRY(stage_queue(S, P, qs));
+        TRY(upload(S));
+        TRY(scatter_queue(S, qs));
+        const int64_t nitems = qs.nitems;
         WaveLaunch w{};
+        w.tag_base = tag_base;
         w.X = c.xp.p;
         w.Y = c.yp.p;
         w.dp = dp;
         w.wide = dpl.wide;
         w.precision = prec;
-        w.passes = S.passes.as<PassDesc>();
+        w.passes = S.dev<PassDesc>(S.passes_off);
         w.items = S.items.as<WorkItem>();
         w.nitems = (int)nitems;
         w.counter = S.counter.as<int>();
         w.out = out_base ? out_base : S.out.p;
-        w.wins = S.wins.as<WinDesc>();
+        w.wins = wins_off == npos ? nullptr : S.dev<WinDesc>(wins_off);
         w.bnd = S.bnd.p;
         w.bp = c.bp.as<unsigned long long>();
         w.lb = S.lb.p;
@@ -672,8 +769,7 @@ struct Engine {
         // level has tiles per pipeline -> half the pipelines per SM, so the
         // head strips run with more of their SM (LMDTW_ACTIVE_NP overrides).
         {
-            int nsm = 148;
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
+            const int nsm = c.nsm;
             const int np = pipes_per_cta(prec, dpl, lat);
             int64_t head = 0;
             for (const auto& p : P) head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
@@ -931,25 +1027,19 @@ struct Engine {
             CU(S.out.ensure((size_t)std::max<int64_t>(out_total, 1) * esz));
             out_base = S.out.p;
         }
-        CU(S.wins.ensure(std::max<size_t>(W.size(), 1) * sizeof(WinDesc)));
-        if (!W.empty()) {  // through pinned staging: a pageable copy would block the host
-            CU(S.h_wins.ensure(W.size() * sizeof(WinDesc)));
-            memcpy(S.h_wins.p, W.data(), W.size() * sizeof(WinDesc));
-            CU(cudaMemcpyAsync(S.wins.p, S.h_wins.p, W.size() * sizeof(WinDesc), cudaMemcpyHostToDevice, S.st));
-        }
+        // one upload for the batch: windows and pivot descriptors ride with
+        // run_wave's pass descriptors and queue input
         (void)cells;
-        TRY(run_wave(S, P, bnd_total, false, nullptr, nullptr, computed));
-        CU(S.pdesc.ensure(V.size() * sizeof(PivotDesc)));
+        const size_t wins_off = W.empty() ? npos : S.stg.add(W.data(), W.size() * sizeof(WinDesc));
+        const size_t pdesc_off = S.stg.add(V.data(), V.size() * sizeof(PivotDesc));
+        TRY(run_wave(S, P, bnd_total, false, nullptr, nullptr, computed, wins_off));
         CU(S.pout.ensure(V.size() * sizeof(PivotOut)));
-        CU(S.h_pdesc.ensure(V.size() * sizeof(PivotDesc)));
         CU(S.h_pout.ensure(V.size() * sizeof(PivotOut)));
-        memcpy(S.h_pdesc.p, V.data(), V.size() * sizeof(PivotDesc));
-        CU(cudaMemcpyAsync(S.pdesc.p, S.h_pdesc.p, V.size() * sizeof(PivotDesc), cudaMemcpyHostToDevice, S.st));
         const size_t scb = pivot_scratch_bytes((int)V.size());
         CU(S.pscratch.ensure(scb));
-        CU(cudaMemsetAsync(S.pscratch.p, 0, scb, S.st));  // zeroes the per-node done counters
-        TRY(launched(launch_pivots(prec, S.passes.as<PassDesc>(), S.pdesc.as<PivotDesc>(), (int)V.size(), out_base,
-                                   S.pout.as<PivotOut>(), S.pscratch.p, S.st),
+        CU(S.pdone.ensure_init(V.size() * sizeof(unsigned), 0, S.st));  // the kernel leaves them at zero
+        TRY(launched(launch_pivots(prec, S.dev<PassDesc>(S.passes_off), S.dev<PivotDesc>(pdesc_off), (int)V.size(),
+                                   out_base, S.pout.as<PivotOut>(), S.pscratch.p, S.pdone.as<unsigned>(), S.st),
                      "pivot_kernel"));
         CU(cudaMemcpyAsync(S.h_pout.p, S.pout.p, V.size() * sizeof(PivotOut), cudaMemcpyDeviceToHost, S.st));
         c.d2h += V.size() * sizeof(PivotOut);
@@ -1033,30 +1123,26 @@ struct Engine {
             cells += nd.M * nd.N;
         }
         CU(c.bp.ensure((size_t)std::max<int64_t>(bp_total, 1) * 8));
-        CU(c.lcost.ensure((size_t)n * esz));
+        auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+        c.lo_pcost = al((size_t)path_total * 2 * sizeof(int));
+        c.lo_plen = c.lo_pcost + al((size_t)path_total * esz);
+        c.lo_lcost = c.lo_plen + al((size_t)n * sizeof(int));
+        const size_t lbytes = c.lo_lcost + (size_t)n * esz;
+        CU(c.lout.ensure(lbytes));
+        CU(c.h_lout.ensure(lbytes));
+        char* lo = c.lout.as<char>();
         void* tab_dev = nullptr;
         if (tab_host) {
             CU(c.tab.ensure((size_t)all[leafs[0]].M * all[leafs[0]].N * esz));
             tab_dev = c.tab.p;
         }
-        TRY(run_wave(c.main, P, bnd_total, true, tab_dev, c.lcost.p, cells));
-        CU(c.ldesc.ensure(n * sizeof(LeafDesc)));
-        CU(cudaMemcpyAsync(c.ldesc.p, L.data(), n * sizeof(LeafDesc), cudaMemcpyHostToDevice, c.st));
-        CU(c.path.ensure((size_t)path_total * 2 * sizeof(int)));
-        CU(c.pcost.ensure((size_t)path_total * esz));
-        CU(c.plen.ensure((size_t)n * sizeof(int)));
-        TRY(launched(launch_backtrace(prec, dpl, c.xp.p, c.yp.p, c.ldesc.as<LeafDesc>(), n,
-                                      c.bp.as<unsigned long long>(), c.path.as<int>(), c.pcost.p, c.plen.as<int>(),
-                                      c.st),
+        const size_t ldesc_off = c.main.stg.add(L.data(), n * sizeof(LeafDesc));  // uploaded with the fill's batch
+        TRY(run_wave(c.main, P, bnd_total, true, tab_dev, lo + c.lo_lcost, cells));
+        TRY(launched(launch_backtrace(prec, dpl, c.xp.p, c.yp.p, c.main.dev<LeafDesc>(ldesc_off), n,
+                                      c.bp.as<unsigned long long>(), reinterpret_cast<int*>(lo), lo + c.lo_pcost,
+                                      reinterpret_cast<int*>(lo + c.lo_plen), c.st),
                      "backtrace_kernel"));
-        CU(c.h_path.ensure((size_t)path_total * 2 * sizeof(int)));
-        CU(c.h_pcost.ensure((size_t)path_total * esz));
-        CU(c.h_plen.ensure((size_t)n * sizeof(int)));
-        CU(c.h_lcost.ensure((size_t)n * esz));
-        CU(cudaMemcpyAsync(c.h_path.p, c.path.p, (size_t)path_total * 2 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
-        CU(cudaMemcpyAsync(c.h_pcost.p, c.pcost.p, (size_t)path_total * esz, cudaMemcpyDeviceToHost, c.st));
-        CU(cudaMemcpyAsync(c.h_plen.p, c.plen.p, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, c.st));
-        CU(cudaMemcpyAsync(c.h_lcost.p, c.lcost.p, (size_t)n * esz, cudaMemcpyDeviceToHost, c.st));
+        CU(cudaMemcpyAsync(c.h_lout.p, lo, lbytes, cudaMemcpyDeviceToHost, c.st));
         c.d2h += (long long)path_total * (2 * sizeof(int) + esz) + n * (sizeof(int) + esz);
         if (tab_host) {
             const size_t tb = (size_t)all[leafs[0]].M * all[leafs[0]].N * esz;
@@ -1065,7 +1151,7 @@ struct Engine {
         }
         CU(cudaStreamSynchronize(c.st));
         c.prof_collect();
-        plen.assign(c.h_plen.as<int>(), c.h_plen.as<int>() + n);
+        plen.assign(c.hplen(), c.hplen() + n);
         for (int q = 0; q < n; q++)
             if (plen[q] < 0) {
                 const Node& nd = all[leafs[q]];
@@ -1078,7 +1164,7 @@ struct Engine {
     }
 
     double leaf_cost(int q) const {
-        return prec == 32 ? (double)c.h_lcost.as<float>()[q] : c.h_lcost.as<double>()[q];
+        return prec == 32 ? (double)c.hlcost<float>()[q] : c.hlcost<double>()[q];
     }
 };
 
@@ -1337,7 +1423,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     TRY(E.leaves(nodes, leafs, xb, yb, nullptr, poff, plen));
     phase("leaves done");
 
-    const int* hpath = c->h_path.as<int>();
+    const int* hpath = c->hpath();
     results.assign(npairs, nullptr);
     struct PhaseEnd {
         std::function<void()> f;
@@ -1398,7 +1484,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
         }
         // cost: sequential sum over the path in order (core.py:191-197)
         if (cfg.precision == 32) {
-            const float* pc = c->h_pcost.as<float>();
+            const float* pc = c->hpcost<float>();
             float total = 0.0f;
             for (size_t s = 0; s < leaf_seq.size(); s++) {
                 const int lf = leaf_seq[s];
@@ -1406,7 +1492,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
             }
             res->info.cost = (double)total;
         } else {
-            const double* pc = c->h_pcost.as<double>();
+            const double* pc = c->hpcost<double>();
             double total = 0.0;
             for (size_t s = 0; s < leaf_seq.size(); s++) {
                 const int lf = leaf_seq[s];
@@ -1611,7 +1697,7 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     pd.sys_out = strip_hi < pd.nstrips ? 1 : 0;  // the next shard may run on a peer GPU
     CU(c->main.out.ensure((size_t)out_total * E.esz));
     CU(c->main.passes.ensure(sizeof(PassDesc)));
-    CU(c->main.counter.ensure(sizeof(int)));
+    CU(c->main.counter.ensure(2 * sizeof(int)));
     CU(c->main.lb.ensure((size_t)pd.nstrips * (H + 1) * E.esz));
     CU(c->main.flags.ensure((size_t)pd.nstrips * sizeof(int)));
     CU(c->main.h_passes.ensure(sizeof(PassDesc)));
@@ -1619,7 +1705,7 @@ int lmdtw_half_pass_shard(int device, const float* X, int64_t M, const float* Y,
     CU(cudaMemcpyAsync(c->main.passes.p, c->main.h_passes.p, sizeof(PassDesc), cudaMemcpyHostToDevice, c->st));
     int64_t nitems = 0;
     TRY(E.upload_queue(c->main, std::vector<PassDesc>{pd}, nitems));
-    CU(cudaMemsetAsync(c->main.counter.p, 0, sizeof(int), c->st));
+    CU(cudaMemsetAsync(c->main.counter.p, 0, 2 * sizeof(int), c->st));
     CU(cudaMemsetAsync(c->main.flags.p, 0, (size_t)pd.nstrips * sizeof(int), c->st));
     WaveLaunch w{};
     w.X = c->xp.p;
@@ -1761,7 +1847,7 @@ int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const f
         E.make_items(c->main, std::vector<PassDesc>{z.pd}, z.items);
         if (z.bnd.ensure((size_t)bnd_total * 8) != cudaSuccess || z.out.ensure((size_t)out_total * E.esz) ||
             z.passes.ensure(sizeof(PassDesc)) || z.items_d.ensure(z.items.size() * sizeof(WorkItem)) ||
-            z.counter.ensure(sizeof(int)) || z.lb.ensure((size_t)S * (H + 1) * E.esz) ||
+            z.counter.ensure(2 * sizeof(int)) || z.lb.ensure((size_t)S * (H + 1) * E.esz) ||
             z.flags.ensure((size_t)S * sizeof(int)) || cudaStreamCreateWithFlags(&z.st, cudaStreamNonBlocking))
             rc = set_err(LMDTW_ENOMEM, "sharded half pass: allocation failed");
     }
@@ -1772,7 +1858,7 @@ int lmdtw_debug_sharded_half_pass(int device, const float* X, int64_t M, const f
             z.pd.sys_out = q + 1 < ns ? 1 : 0;
             cudaMemcpy(z.passes.p, &z.pd, sizeof(PassDesc), cudaMemcpyHostToDevice);
             cudaMemcpy(z.items_d.p, z.items.data(), z.items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice);
-            cudaMemset(z.counter.p, 0, sizeof(int));
+            cudaMemset(z.counter.p, 0, 2 * sizeof(int));
             cudaMemset(z.bnd.p, 0xFF, (size_t)bnd_total * 8);  // tag -1
             cudaMemset(z.flags.p, 0, (size_t)S * sizeof(int));
         }
@@ -1917,7 +2003,7 @@ int lmdtw_dtw_full(int device, const float* X, int64_t M, const float* Y, int64_
     std::vector<int64_t> poff;
     std::vector<int> plen;
     TRY(E.leaves(nodes, std::vector<int>{0}, xb, yb, D_out, poff, plen));
-    const int* lp = c->h_path.as<int>();
+    const int* lp = c->hpath();
     const int len = plen[0];
     for (int q = 0; q < len; q++) {
         path_out[2 * q] = lp[2 * (len - 1 - q)];
@@ -2027,7 +2113,7 @@ int lmdtw_leaf_nodes(int device, const float* X, int64_t M, const float* Y, int6
     std::vector<int64_t> poff;
     std::vector<int> plen;
     TRY(E.leaves(nodes, ids, xb, yb, nullptr, poff, plen));
-    const int* hp = c->h_path.as<int>();
+    const int* hp = c->hpath();
     int64_t w = 0;
     for (int q = 0; q < n; q++) {
         const int len = plen[q];
@@ -2110,9 +2196,9 @@ int lmdtw_pivot_combine_device(int device, int32_t precision, int64_t M, int64_t
     CU(cudaMemcpyAsync(c->main.pdesc.p, &v, sizeof v, cudaMemcpyHostToDevice, c->st));
     const size_t scb = pivot_scratch_bytes(1);
     CU(c->main.pscratch.ensure(scb));
-    CU(cudaMemsetAsync(c->main.pscratch.p, 0, scb, c->st));
+    CU(c->main.pdone.ensure_init(sizeof(unsigned), 0, c->st));  // the kernel leaves it at zero
     CU(launch_pivots(precision, c->main.passes.as<PassDesc>(), c->main.pdesc.as<PivotDesc>(), 1, c->main.out.p,
-                     c->main.pout.as<PivotOut>(), c->main.pscratch.p, c->st));
+                     c->main.pout.as<PivotOut>(), c->main.pscratch.p, c->main.pdone.as<unsigned>(), c->st));
     g_launches++;
     PivotOut po{};
     CU(cudaMemcpyAsync(&po, c->main.pout.p, sizeof po, cudaMemcpyDeviceToHost, c->st));

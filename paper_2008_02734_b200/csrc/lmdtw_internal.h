@@ -110,7 +110,9 @@ struct WaveLaunch {
     const PassDesc* passes;
     const WorkItem* items;
     int nitems;
-    int* counter;           // work queue head (zeroed by caller)
+    int* counter;           // [0] work queue head, [1] exit count: zero before the first launch
+                            // on the buffer; the kernel leaves both at zero
+    int tag_base;           // strip handoff tags are tag_base + strip (see Engine::next_tags)
     void* out;              // half-pass diagonal outputs
     void* bnd;              // strip handoff words (memset 0xFF = tag -1 by caller)
     unsigned long long* bp; // leaf backpointers
@@ -154,8 +156,9 @@ cudaError_t set_watchdog_ns_f64(unsigned long long ns);
 cudaError_t launch_scatter_items(const StripEnt* ents, int nents, int32_t* cursor, int key_per_tile,
                                  WorkItem* items, cudaStream_t stream);
 cudaError_t launch_pivots(int precision, const PassDesc* passes, const PivotDesc* piv, int npiv,
-                          const void* out, PivotOut* res, void* scratch, cudaStream_t stream);
-// scratch for launch_pivots; its per-node counters must start at zero
+                          const void* out, PivotOut* res, void* scratch, unsigned* done, cudaStream_t stream);
+// scratch for launch_pivots; `done` holds npiv counters that must be zero on
+// entry (the kernel leaves them at zero)
 size_t pivot_scratch_bytes(int npiv);
 cudaError_t launch_backtrace(int precision, DimPlan dp, const void* X, const void* Y, const LeafDesc* leaves,
                              int nleaves, const unsigned long long* bp, int* path, void* pcost,
