@@ -555,9 +555,7 @@ struct Engine {
         // concatenated series lives at padded row kPadRows + r.
         const size_t rowb = (size_t)dp * esz;
         CU(pad.ensure((size_t)(total + 2 * kPadRows) * rowb));
-        CU(cudaMemsetAsync(pad.p, 0, kPadRows * rowb, c.st));
-        CU(cudaMemsetAsync((char*)pad.p + (kPadRows + total) * rowb, 0, kPadRows * rowb, c.st));
-        char* body = (char*)pad.p + kPadRows * rowb;
+        char* body = (char*)pad.p + kPadRows * rowb;  // the guard rows: the first / last cast launch
         if (mem == LMDTW_MEM_HOST) {
             CU(raw.ensure((size_t)total * d * sizeof(float)));
             for (int p = 0; p < n; p++) {
@@ -565,11 +563,14 @@ struct Engine {
                                    cudaMemcpyHostToDevice, c.st));
                 c.h2d += (long long)rows[p] * d * sizeof(float);
             }
-            TRY(launched(launch_pad_cast(prec, raw.as<float>(), total, d, dp, body, c.st), "pad_cast"));
+            TRY(launched(launch_pad_cast(prec, raw.as<float>(), total, d, dp, body, c.st, kPadRows, kPadRows),
+                         "pad_cast"));
         } else {
             for (int p = 0; p < n; p++) {
                 char* dst = body + (size_t)base[p] * rowb;
-                TRY(launched(launch_pad_cast(prec, src[p], rows[p], d, dp, dst, c.st), "pad_cast"));
+                TRY(launched(launch_pad_cast(prec, src[p], rows[p], d, dp, dst, c.st, p == 0 ? kPadRows : 0,
+                                             p == n - 1 ? kPadRows : 0),
+                             "pad_cast"));
             }
         }
         for (int p = 0; p < n; p++) base[p] += kPadRows;
@@ -1291,9 +1292,12 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
         const int v = e ? atoi(e) : 1;
         return v < 1 ? 1 : (v > 32 ? 32 : v);
     }();
-    cudaEvent_t staged;
-    CU(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
-    CU(cudaEventRecord(staged, c->st));  // features padded and cast
+    // features padded and cast on c->st; batch slots on other streams wait for it
+    cudaEvent_t staged = nullptr;
+    if (kMaxFlights > 1) {
+        CU(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
+        CU(cudaEventRecord(staged, c->st));
+    }
     struct Flight {
         Slot* S;
         std::vector<int> ids;
@@ -1315,7 +1319,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     for (int k = kMaxFlights - 1; k >= 0; k--) {
         Slot* s = slot_for(k);
         if (!s) {
-            cudaEventDestroy(staged);
+            if (staged) cudaEventDestroy(staged);
             return cuda_err(cudaGetLastError(), "batch stream");
         }
         free_slots.push_back(s);
@@ -1349,7 +1353,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
                 free_slots.pop_back();
                 std::sort(g.begin(), g.end());
                 f.ids = g;
-                if (cudaStreamWaitEvent(f.S->st, staged, 0) != cudaSuccess) {
+                if (staged && f.S->st != c->st && cudaStreamWaitEvent(f.S->st, staged, 0) != cudaSuccess) {
                     rc = cuda_err(cudaGetLastError(), "cudaStreamWaitEvent");
                     break;
                 }
@@ -1413,7 +1417,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     }
     // on error: drain what is in flight before the buffers are reused
     for (auto& f : flights) cudaEventSynchronize(f.S->done);
-    cudaEventDestroy(staged);
+    if (staged) cudaEventDestroy(staged);
     if (rc != LMDTW_OK) return rc;
     c->prof_collect();
     // leaves, in node order (the stitching below walks the tree)

@@ -163,8 +163,10 @@ size_t pivot_scratch_bytes(int npiv);
 cudaError_t launch_backtrace(int precision, DimPlan dp, const void* X, const void* Y, const LeafDesc* leaves,
                              int nleaves, const unsigned long long* bp, int* path, void* pcost,
                              int* plen, cudaStream_t stream);
+// rows of src (float32, d columns) cast to the dtype and padded to dp
+// columns at dst; `pre` zero rows before and `post` after are written too
 cudaError_t launch_pad_cast(int precision, const float* src, int64_t rows, int d, int dp, void* dst,
-                            cudaStream_t stream);
+                            cudaStream_t stream, int pre = 0, int post = 0);
 int max_resident_warps(int precision, DimPlan dp, int leaf, int device, int lat = 0);
 
 // ---- window.cu: windowed DP (approx._window_fill), path costs, discrepancy
