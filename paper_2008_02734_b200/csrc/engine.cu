@@ -34,7 +34,7 @@ using namespace lmdtw;
 
 struct lmdtw_result {
     lmdtw_align_info_t info;
-    std::vector<int64_t> path;
+    std::unique_ptr<int64_t[]> path;  // 2 * info.path_len, written once (no zero fill)
     std::vector<lmdtw_pivot_t> pivots;
 };
 
@@ -1465,45 +1465,31 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
             stack.push_back(n.right);
             stack.push_back(n.left);
         }
-        // path: leaf paths in order, first cell of every later leaf dropped
-        std::vector<const void*> cparts;
-        std::vector<int> clens;
+        // path: leaf paths in order, first cell of every later leaf dropped;
+        // cost: the sequential sum over the path in that order (core.py:191-197)
+        // -- one pass, so the add chain's latency hides the path writes
         int64_t K = 0;
         for (size_t s = 0; s < leaf_seq.size(); s++) K += plen[leaf_seq[s]] - (s ? 1 : 0);
-        res->path.resize(2 * K);
-        int64_t w = 0;
-        std::vector<const float*> cf;
-        std::vector<const double*> cd;
-        for (size_t s = 0; s < leaf_seq.size(); s++) {
-            const int lf = leaf_seq[s];
-            const Node& n = nodes[leafs[lf]];
-            const int len = plen[lf];
-            const int* lp = hpath + 2 * poff[lf];  // reversed: lp[0] is the corner
-            const int skip = s ? 1 : 0;
-            for (int q = len - 1 - skip; q >= 0; q--) {
-                res->path[2 * w] = n.i_off + lp[2 * q];
-                res->path[2 * w + 1] = n.j_off + lp[2 * q + 1];
-                w++;
-            }
-        }
-        // cost: sequential sum over the path in order (core.py:191-197)
-        if (cfg.precision == 32) {
-            const float* pc = c->hpcost<float>();
-            float total = 0.0f;
+        res->path.reset(new int64_t[std::max<int64_t>(2 * K, 1)]);
+        auto build = [&](auto zero, const auto* pc) {
+            auto total = zero;
+            int64_t* out = res->path.get();
             for (size_t s = 0; s < leaf_seq.size(); s++) {
                 const int lf = leaf_seq[s];
-                for (int q = plen[lf] - 1 - (s ? 1 : 0); q >= 0; q--) total = total + pc[poff[lf] + q];
+                const Node& n = nodes[leafs[lf]];
+                const int* lp = hpath + 2 * poff[lf];  // reversed: lp[0] is the corner
+                const auto* cl = pc + poff[lf];
+                const int64_t io = n.i_off, jo = n.j_off;
+                for (int q = plen[lf] - 1 - (s ? 1 : 0); q >= 0; q--) {
+                    out[0] = io + lp[2 * q];
+                    out[1] = jo + lp[2 * q + 1];
+                    out += 2;
+                    total = total + cl[q];
+                }
             }
-            res->info.cost = (double)total;
-        } else {
-            const double* pc = c->hpcost<double>();
-            double total = 0.0;
-            for (size_t s = 0; s < leaf_seq.size(); s++) {
-                const int lf = leaf_seq[s];
-                for (int q = plen[lf] - 1 - (s ? 1 : 0); q >= 0; q--) total = total + pc[poff[lf] + q];
-            }
-            res->info.cost = total;
-        }
+            return (double)total;
+        };
+        res->info.cost = cfg.precision == 32 ? build(0.0f, c->hpcost<float>()) : build(0.0, c->hpcost<double>());
         if (in.cb) in.cb(in.cells, in.budget, in.user);
         res->info.path_len = K;
         res->info.cells_processed = in.cells;
@@ -2222,7 +2208,7 @@ int lmdtw_result_info(const lmdtw_result_t* r, lmdtw_align_info_t* info) {
 
 int lmdtw_result_path(const lmdtw_result_t* r, int64_t* path_out) {
     if (!r || !path_out) return set_err(LMDTW_EINVAL, "null result");
-    memcpy(path_out, r->path.data(), r->path.size() * sizeof(int64_t));
+    if (r->info.path_len > 0) memcpy(path_out, r->path.get(), (size_t)r->info.path_len * 2 * sizeof(int64_t));
     return LMDTW_OK;
 }
 
