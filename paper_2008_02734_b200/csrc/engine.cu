@@ -1419,7 +1419,7 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
     for (auto& f : flights) cudaEventSynchronize(f.S->done);
     if (staged) cudaEventDestroy(staged);
     if (rc != LMDTW_OK) return rc;
-    c->prof_collect();
+    if (leafs.empty()) c->prof_collect();  // else leaves() collects after its sync (off the critical path)
     // leaves, in node order (the stitching below walks the tree)
     std::vector<int64_t> poff;
     std::vector<int> plen;
