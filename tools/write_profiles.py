@@ -76,7 +76,10 @@ for c, path in [("cfg1", "cfg_cfg1.json"), ("cfg2", "cfg_cfg2.json"), ("cfg3", "
     res.append({"config": c, "workload": d["config"]["workload"], "dtype": d["dtype"], "GCUPS": d["value"],
                 "ms_per_step": d["ms_per_step"], "sec_per_alignment": d["config"]["sec_per_alignment"],
                 "e2e_GCUPS": d["e2e"]["value"], "wave_kernel_Gcell_s": d["roofline"]["achieved"],
-                "roofline_frac_fp32_slots": d["roofline"]["frac"], "clocks": d.get("clocks"),
+                "roofline_frac_fp32_slots": d["roofline"]["frac"],
+                "wave_kernel_computed_Gcell_s": d["roofline"].get("achieved_computed"),
+                "frac_computed": d["roofline"].get("frac_computed"),
+                "frac_alignment": d["roofline"].get("frac_alignment"), "clocks": d.get("clocks"),
                 "cells_per_step": d["config"]["cells_per_step"],
                 "cells_computed_per_step": d["config"].get("cells_computed_per_step")})
 ref = last_json(os.path.join(G, "final_reference.json"))
