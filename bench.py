@@ -259,10 +259,14 @@ def numba_reference_cfg2():
         f"sys.path.insert(0, {ref!r}); sys.path.insert(1, {ROOT!r})\n"
         "import lmdtw, bench\n"
         "X, Y = bench.make_inputs('cfg1')[0]\n"
-        "lmdtw.linmdtw(X, Y, precision=32)\n"
+        "lmdtw.linmdtw(X, Y, precision=32); lmdtw.linmdtw(X, Y, precision=64)\n"
+        "t = time.perf_counter()\n"
+        "for _ in range(10): r1 = lmdtw.linmdtw(X, Y, precision=64)\n"
+        "dt1 = (time.perf_counter() - t) / 10\n"
         "X, Y = bench.make_inputs('cfg2')[0]\n"
         "t = time.perf_counter(); r = lmdtw.linmdtw(X, Y, precision=32); dt = time.perf_counter() - t\n"
-        "print(json.dumps({'cells': int(r.cells_processed), 'secs': dt, 'cost': float(r.cost)}))\n")
+        "print(json.dumps({'cells': int(r.cells_processed), 'secs': dt, 'cost': float(r.cost),\n"
+        "                  'cells1': int(r1.cells_processed), 'secs1': dt1, 'cost1': float(r1.cost)}))\n")
     env = dict(os.environ, NUMBA_CACHE_DIR="/tmp/lmdtw_numba_cache", PYTHONDONTWRITEBYTECODE="1")
     try:
         out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240,
@@ -272,7 +276,10 @@ def numba_reference_cfg2():
         return None
     return {"value": round(r["cells"] / r["secs"] / 1e9, 4), "unit": "GCUPS", "cores": 1, "kind": "reference",
             "seconds": round(r["secs"], 2), "cost": r["cost"],
-            "sample": "unmodified reference lmdtw.linmdtw (baseline/_ref, numba) on cfg2 20000x20000 d=12 fp32"}
+            "sample": "unmodified reference lmdtw.linmdtw (baseline/_ref, numba) on cfg2 20000x20000 d=12 fp32",
+            "cfg1": {"sec_per_alignment": round(r["secs1"], 5), "GCUPS": round(r["cells1"] / r["secs1"] / 1e9, 4),
+                     "cost": r["cost1"], "reps": 10,
+                     "sample": "the same reference on cfg1 (1000x1000 d=2 random walks, fp64), mean of 10"}}
 
 
 def cpu_desc():
