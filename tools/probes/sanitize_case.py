@@ -22,8 +22,9 @@ if what == "align":
         r = L.linmdtw(X, Y, min_dim=200, precision=prec)
         print("align", prec, r.cost, len(r.pivot_trace))
     Xw, Yw = bench.latent_pair(500, 450, 100, seed=4)
-    r = L.linmdtw(Xw, Yw, min_dim=200, precision=64)
-    print("align wide", r.cost)
+    for prec in (32, 64):  # WIDE kernels (cp.async-staged X / Y blocks)
+        r = L.linmdtw(Xw, Yw, min_dim=200, precision=prec)
+        print("align wide", prec, r.cost)
 else:
     lib = _capi.load()
     M, N, d = 700, 600, 12
