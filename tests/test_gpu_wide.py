@@ -66,3 +66,26 @@ def test_wide_find_pivot_vs_oracle():
             o = O.find_pivot(X, Y, prec, rule)
             assert (p.i, p.j, p.diagonal_k, p.total_at_pivot) == (o["i"], o["j"], o["diagonal_k"],
                                                                  o["total_at_pivot"])
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_wide_multi_tile_vs_oracle(prec):
+    """Passes longer than one 8192-column tile on the WIDE kernels: tile
+    boundaries (left-boundary handoff between tiles of a strip), the static
+    first round of work items and the cp.async-staged X / Y blocks across
+    tiles; a half pass in both directions and a skinny brute-force leaf."""
+    d = 100
+    X, Y = rnd(700, d, 3, "walk"), rnd(18000, d, 4, "walk")
+    kstop = (700 + 18000) // 2
+    for direction in ("forward", "reverse"):
+        b = L.diag_dtw(X, Y, kstop, direction, precision=prec)
+        od, oc, cells = O.half_pass(X, Y, kstop, direction, prec)
+        for s in range(3):
+            assert np.array_equal(b.d[s], od[s]), (direction, s)
+            assert np.array_equal(b.c[s], oc[s])
+        assert b.cells_processed == cells
+    Xs = X[:40]
+    r = L.dtw_full(Xs, Y, tie_rule=PERMS[0], precision=prec)
+    c, p = O.dtw_full(Xs, Y, PERMS[0], prec)
+    assert r.cost == c
+    assert np.array_equal(r.path, p)
