@@ -249,13 +249,16 @@ def cpu_run(name, pairs, nthreads, min_dim=500):
 
 def numba_reference_cfg2():
     """The real reference (Python + numba, installed unmodified in
-    baseline/_ref) on cfg2 in fp32, one core (numba holds the GIL), JIT warmed
-    on cfg1 first.  None when it cannot be imported on this host."""
+    baseline/_ref), JIT warmed on cfg1 first, SURVEY.md 8(d)'s repetitions
+    where they fit a bench run: cfg1 x10 (fp64), cfg2 x3 (fp32, one core --
+    numba holds the GIL), and cfg4 as an all-core multiprocessing pool (one
+    pair per task) over the first 32 pairs.  None when it cannot be
+    imported on this host."""
     ref = os.path.join(ROOT, "baseline", "_ref")
     if not os.path.isdir(os.path.join(ref, "lmdtw")):
         return None
     code = (
-        "import sys, time, json\n"
+        "import sys, time, json, os, multiprocessing as mp\n"
         f"sys.path.insert(0, {ref!r}); sys.path.insert(1, {ROOT!r})\n"
         "import lmdtw, bench\n"
         "X, Y = bench.make_inputs('cfg1')[0]\n"
@@ -264,22 +267,37 @@ def numba_reference_cfg2():
         "for _ in range(10): r1 = lmdtw.linmdtw(X, Y, precision=64)\n"
         "dt1 = (time.perf_counter() - t) / 10\n"
         "X, Y = bench.make_inputs('cfg2')[0]\n"
-        "t = time.perf_counter(); r = lmdtw.linmdtw(X, Y, precision=32); dt = time.perf_counter() - t\n"
-        "print(json.dumps({'cells': int(r.cells_processed), 'secs': dt, 'cost': float(r.cost),\n"
-        "                  'cells1': int(r1.cells_processed), 'secs1': dt1, 'cost1': float(r1.cost)}))\n")
+        "ts = []\n"
+        "for _ in range(3):\n"
+        "    t = time.perf_counter(); r = lmdtw.linmdtw(X, Y, precision=32); ts.append(time.perf_counter() - t)\n"
+        "def work(p):\n"
+        "    return int(lmdtw.linmdtw(p[0], p[1], precision=32).cells_processed)\n"
+        "pairs = bench.make_inputs('cfg4')[:32]\n"
+        "n = os.cpu_count()\n"
+        "with mp.get_context('fork').Pool(n) as pool:\n"
+        "    pool.map(work, [bench.make_inputs('cfg1')[0]] * n, chunksize=1)\n"
+        "    t = time.perf_counter(); c4 = pool.map(work, pairs, chunksize=1); dt4 = time.perf_counter() - t\n"
+        "print(json.dumps({'cells': int(r.cells_processed), 'secs': sorted(ts)[1], 'all': ts, 'cost': float(r.cost),\n"
+        "                  'cells1': int(r1.cells_processed), 'secs1': dt1, 'cost1': float(r1.cost),\n"
+        "                  'cells4': sum(c4), 'secs4': dt4, 'n4': len(pairs), 'procs': n}))\n")
     env = dict(os.environ, NUMBA_CACHE_DIR="/tmp/lmdtw_numba_cache", PYTHONDONTWRITEBYTECODE="1")
     try:
-        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240,
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=420,
                              env=env, cwd="/tmp")
         r = json.loads(out.stdout.strip().splitlines()[-1])
     except Exception:
         return None
     return {"value": round(r["cells"] / r["secs"] / 1e9, 4), "unit": "GCUPS", "cores": 1, "kind": "reference",
-            "seconds": round(r["secs"], 2), "cost": r["cost"],
-            "sample": "unmodified reference lmdtw.linmdtw (baseline/_ref, numba) on cfg2 20000x20000 d=12 fp32",
+            "seconds": round(r["secs"], 2), "seconds_all": [round(v, 2) for v in r["all"]], "cost": r["cost"],
+            "sample": "unmodified reference lmdtw.linmdtw (baseline/_ref, numba) on cfg2 20000x20000 d=12 fp32, "
+                      "median of 3",
             "cfg1": {"sec_per_alignment": round(r["secs1"], 5), "GCUPS": round(r["cells1"] / r["secs1"] / 1e9, 4),
                      "cost": r["cost1"], "reps": 10,
-                     "sample": "the same reference on cfg1 (1000x1000 d=2 random walks, fp64), mean of 10"}}
+                     "sample": "the same reference on cfg1 (1000x1000 d=2 random walks, fp64), mean of 10"},
+            "cfg4": {"GCUPS": round(r["cells4"] / r["secs4"] / 1e9, 4), "seconds": round(r["secs4"], 2),
+                     "pairs_per_s": round(r["n4"] / r["secs4"], 3), "cores": r["procs"],
+                     "sample": f"the same reference on the first {r['n4']} cfg4 pairs, fp32, multiprocessing "
+                               f"pool of {r['procs']} processes, one pair per task (all cores)"}}
 
 
 def cpu_desc():
