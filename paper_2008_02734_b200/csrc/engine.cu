@@ -23,6 +23,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -1433,7 +1434,11 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
         std::function<void()> f;
         ~PhaseEnd() { f(); }
     } phase_end{[&] { phase("results built"); }};
-    for (int p = 0; p < npairs; p++) {
+    // One result per pair; pairs are independent (the inputs are read-only,
+    // inst[p] and results[p] belong to pair p), so a batch builds them on
+    // host threads: the sequential cost sum over each path is a dependent add
+    // chain, ~12 ms over cfg4's 256 paths on one thread.
+    auto build_one = [&](int p) {
         std::unique_ptr<lmdtw_result> res(new lmdtw_result());
         Inst& in = inst[p];
         // pre-order DFS: pivots and leaf sequence
@@ -1502,6 +1507,34 @@ int align_core(int device, int npairs, const float* const* X, const int64_t* M, 
         res->info.h2d_bytes = c->h2d;
         res->info.d2h_bytes = c->d2h;
         results[p] = res.release();
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nth = npairs >= 8 ? (int)std::min<unsigned>(std::min<unsigned>((unsigned)npairs / 4, 16u), hw) : 1;
+    if (nth <= 1) {
+        for (int p = 0; p < npairs; p++) build_one(p);
+        return LMDTW_OK;
+    }
+    std::atomic<int> next{0};
+    std::atomic<bool> failed{false};
+    {
+        std::vector<std::thread> pool;
+        pool.reserve(nth);
+        for (int t = 0; t < nth; t++)
+            pool.emplace_back([&] {
+                try {
+                    for (int p; !failed.load() && (p = next.fetch_add(1)) < npairs;) build_one(p);
+                } catch (...) {
+                    failed.store(true);
+                }
+            });
+        for (auto& t : pool) t.join();
+    }
+    if (failed.load()) {
+        for (auto*& r : results) {
+            delete r;
+            r = nullptr;
+        }
+        return set_err(LMDTW_ENOMEM, "host allocation failed while building the results");
     }
     return LMDTW_OK;
 }
