@@ -92,19 +92,29 @@ def find_pivot(X, Y, cost: str = "euclidean", precision=64, parallel: bool = Fal
                  diagonal_k=int(k.value))
 
 
-def _result(handle, M, N, dtype) -> AlignmentResult:
+# PivotRec (include/lmdtw_b200.h) as a numpy record: one .tolist() instead of
+# ten ctypes attribute reads per pivot
+_PIV_DT = np.dtype([("i", "<i8"), ("j", "<i8"), ("i_off", "<i8"), ("j_off", "<i8"), ("M", "<i8"), ("N", "<i8"),
+                    ("sub_i", "<i8"), ("sub_j", "<i8"), ("diagonal_k", "<i8"), ("total_at_pivot", "<f8")])
+assert _PIV_DT.itemsize == C.sizeof(_capi.PivotRec)
+
+
+def _result(handle, M, N, dtype, path=None) -> AlignmentResult:
+    """The Python result of one C result handle; `path` (optional) is a
+    preallocated (path_len, 2) int64 array to fill."""
     L = _capi.load()
     info = _capi.AlignInfo()
     _capi.check(L.lmdtw_result_info(handle, C.byref(info)))
-    path = np.empty((info.path_len, 2), np.int64)
+    if path is None:
+        path = np.empty((info.path_len, 2), np.int64)
     _capi.check(L.lmdtw_result_path(handle, _capi.ptr(path)))
-    recs = (_capi.PivotRec * max(1, info.n_pivots))()
-    _capi.check(L.lmdtw_result_pivots(handle, recs))
+    recs = np.empty(max(1, info.n_pivots), _PIV_DT)
+    _capi.check(L.lmdtw_result_pivots(handle, _capi.ptr(recs)))
+    # the reference's key order (divide.py:160-164)
     trace = tuple(
-        {"i": r.i, "j": r.j, "i_off": r.i_off, "j_off": r.j_off, "M": r.M, "N": r.N,
-         "sub_i": r.sub_i, "sub_j": r.sub_j, "total_at_pivot": r.total_at_pivot,
-         "diagonal_k": r.diagonal_k}
-        for r in recs[:info.n_pivots])
+        {"i": r[0], "j": r[1], "i_off": r[2], "j_off": r[3], "M": r[4], "N": r[5], "sub_i": r[6], "sub_j": r[7],
+         "total_at_pivot": r[9], "diagonal_k": r[8]}
+        for r in recs[:info.n_pivots].tolist())
     res = AlignmentResult(
         cost=float(info.cost), path=path, cells_processed=int(info.cells_processed),
         cells_budget=2 * M * N, precision=str(dtype), algorithm="linmdtw",
@@ -186,8 +196,18 @@ def align_batch(pairs, cost: str = "euclidean", config: LinMdtwConfig | None = N
                                     _capi.MEM_HOST, handles))
     out = []
     try:
+        # every path in one allocation (one large, hugepage-eligible buffer
+        # instead of n page-faulting small ones); each result holds a view
+        lens = []
         for q in range(n):
-            out.append(_result(C.c_void_p(handles[q]), Ms[q], Ns[q], dtype))
+            info = _capi.AlignInfo()
+            _capi.check(L.lmdtw_result_info(C.c_void_p(handles[q]), C.byref(info)))
+            lens.append(int(info.path_len))
+        paths = np.empty((sum(lens), 2), np.int64)
+        off = 0
+        for q in range(n):
+            out.append(_result(C.c_void_p(handles[q]), Ms[q], Ns[q], dtype, paths[off:off + lens[q]]))
+            off += lens[q]
     finally:
         for q in range(n):
             L.lmdtw_result_free(C.c_void_p(handles[q]))
