@@ -300,6 +300,17 @@ def numba_reference_cfg2():
                                f"pool of {r['procs']} processes, one pair per task (all cores)"}}
 
 
+def host_threads() -> int:
+    """All host threads this process may run on.  Not omp_get_max_threads():
+    torchrun sets OMP_NUM_THREADS=1 in every rank, and the reference arm's
+    rank 0 must still use the whole host (the oracle passes the count to
+    its num_threads clause)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def cpu_desc():
     try:
         model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
@@ -336,7 +347,7 @@ def run_reference(args, rank, world):
         return
     from oracle import oracle as O
     O.build()
-    nthreads = O.num_threads()
+    nthreads = host_threads()
     pairs, desc = cpu_workload(args.config, args.min_dim)
     warm = make_inputs("cfg1")
     for _ in range(args.warmup):
@@ -591,7 +602,7 @@ def run_ours(args, rank, world):
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle as O
-        nthreads = O.num_threads()
+        nthreads = host_threads()
         cpairs, desc = cpu_workload(args.config, args.min_dim)
         g, secs, ncell = cpu_run(args.config, cpairs, nthreads, args.min_dim)
         model, ncpu = cpu_desc()
