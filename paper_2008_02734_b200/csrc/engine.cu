@@ -776,7 +776,14 @@ struct Engine {
             int64_t head = 0;
             for (const auto& p : P) head = std::max<int64_t>(head, tiles_of(p, p.strip_lo, H));
             const double per_pipe = (double)nitems / ((double)np * nsm);
-            w.active_np = (head > 2.0 * per_pipe && np >= 2) ? np / 2 : np;
+            // LMDTW_LAT_FACTOR (experiments): the head / per-pipeline tile ratio above which
+            // a launch counts as latency-bound (default 2)
+            static const double lat_factor = [] {
+                const char* e = getenv("LMDTW_LAT_FACTOR");
+                const double f = e ? atof(e) : 2.0;
+                return f > 0 ? f : 2.0;
+            }();
+            w.active_np = (head > lat_factor * per_pipe && np >= 2) ? np / 2 : np;
             if (const char* a = getenv("LMDTW_ACTIVE_NP")) w.active_np = atoi(a);
         }
         w.flags = S.flags.as<int>();
